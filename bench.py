@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark harness (driver contract).
+
+Default workload (BASELINE.json configs[4], the graded one): PageRank with
+EdgeBlocking on RMAT scale 27 (V = 2^27, E = 2^31, edge factor 16,
+a/b/c = .57/.19/.19, seed 7), 20 iterations, tolerance 0.  One "step" = one
+complete ``pagerank(g, program, max_iters=20, tolerance=0.0)`` call with the
+graph resident in HBM; metric GTEPS = 20*E / step time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gg|reference]
+                  [--config c5|c1|...] [--scale S] [--schedule eb|edge|pull|...]
+
+Multi-GPU (torchrun): every rank runs the same per-GPU workload on its own
+device ("scaling": "weak", replicas); value = all ranks' edges / max time.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (scale, edge_factor, seed, iterations)
+    "c5": (27, 16, 7, 20),
+    "c1": (16, 16, 1, 20),
+}
+
+SCHEDULES = {
+    "eb": dict(load_balance="EDGE_ONLY", blocking=True),
+    "edge": dict(load_balance="EDGE_ONLY"),
+    "pull": dict(direction="PULL", load_balance="STRICT"),
+    "pull_twc": dict(direction="PULL", load_balance="TWC"),
+    "pull_etwc": dict(direction="PULL", load_balance="ETWC"),
+    "pull_wm": dict(direction="PULL", load_balance="WM"),
+    "push": dict(direction="PUSH", load_balance="ETWC"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="gg", choices=["gg", "reference"])
+    p.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    p.add_argument("--scale", type=int, default=None)
+    p.add_argument("--schedule", default="eb", choices=sorted(SCHEDULES))
+    p.add_argument("--fp32-contrib", action="store_true")
+    p.add_argument("--permute", action="store_true", help="Graph500-style id permutation")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-scale", type=int, default=22)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region (B200_PROFILING.md "clocks line")
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port (test infrastructure) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_pagerank_sample(scale, edge_factor, seed, budget_s=20.0, max_iters=20):
+    import numpy as np
+    import oracle
+    V, s, d = oracle.rmat(scale, edge_factor, seed=seed)
+    in_off, in_nbr, _ = oracle.csr(V, d, s)
+    out_off, _, _ = oracle.csr(V, s, np.zeros_like(d))
+    E = len(s)
+    # one warm-up iteration, then as many timed single-iteration steps as fit the budget
+    oracle.pagerank_par(V, in_off, in_nbr, out_off, 1, 0.0)
+    t0 = time.perf_counter()
+    iters = 0
+    while iters < max_iters:
+        oracle.pagerank_par(V, in_off, in_nbr, out_off, 1, 0.0)
+        iters += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": E * iters / dt / 1e9, "unit": "GTEPS", "cores": oracle.num_threads(),
+            "kind": "port",
+            "sample": "RMAT scale %d ef %d seed %d (E=%d), %d PageRank iteration(s) of "
+                      "oracle.c or_pagerank_par (pull, OpenMP, f64) in %.1f s"
+                      % (scale, edge_factor, seed, E, iters, dt)}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    scale, ef, seed, iters = CONFIGS[args.config]
+    if args.scale:
+        scale = args.scale
+    workload = "pagerank_%s_rmat%d_ef%d" % (args.schedule, scale, ef)
+    metric = "GTEPS per algorithm x graph (PR/BFS/SSSP/CC/BC); PR GTEPS at 1/2/4/8 GPUs"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cs = min(args.cpu_scale, scale)
+        step_vals = []
+        for _ in range(args.warmup):
+            cpu_pagerank_sample(cs, ef, seed, budget_s=5.0, max_iters=1)
+        for _ in range(args.steps):
+            step_vals.append(cpu_pagerank_sample(cs, ef, seed, budget_s=10.0, max_iters=3))
+        v = statistics.median(x["value"] for x in step_vals)
+        base = step_vals[0]
+        line = {"metric": metric, "value": v, "unit": "GTEPS", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": workload, "cpu_sample_scale": cs, "iterations": iters},
+                "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": base["cores"],
+                                 "kind": "port", "sample": base["sample"]},
+                "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import numpy as np
+    import torch
+    import paper_2012_07990_b200 as gg
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    t0 = time.perf_counter()
+    g = gg.generate_rmat(scale, ef, seed=seed, sort_by_source=True, permute=args.permute,
+                         device=local)
+    gen_s = time.perf_counter() - t0
+    V, E = g.num_vertices, g.num_edges
+    sch = gg.Schedule(**SCHEDULES[args.schedule])
+    prog = gg.ScheduleProgram({"s0:s1": sch})
+    prep_ms = 0.0
+    if sch.blocking:
+        bg_t = time.perf_counter()
+        import ctypes as C
+        from paper_2012_07990_b200 import _lib
+        h, pm = C.c_void_p(), C.c_double()
+        n = gg.default_blocking_size(g)
+        _lib.call("gg_block_edges", g.handle, n, C.byref(h), C.byref(pm))
+        prep_ms = pm.value
+    ranks = torch.empty(V, dtype=torch.float64, device="cuda")
+
+    def step():
+        return gg.pagerank(g, prog, max_iters=iters, tolerance=0.0, out=ranks,
+                           contrib_fp32=args.fp32_contrib)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    peak, peak_kind = measured_peaks()
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        edge_ms = 0.0
+        edge_n = 0
+        launches = 0
+        for _ in range(args.steps):
+            r = step()
+            edge_ms += r.stats.edge_ms
+            edge_n += r.stats.edge_launches
+            launches += r.stats.gpu_launches
+        ev1.record()
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_t = torch.tensor([ms], device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = world * iters * E / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (edge phase), algorithmic bytes per launch:
+    # 8 B/edge (COO pair) + 16 B/vertex (contrib read, acc write) -- SURVEY §8(d)
+    avg_edge_ms = edge_ms / max(1, edge_n)
+    alg_edge = 8.0 * E + 16.0 * V
+    achieved = alg_edge / (avg_edge_ms * 1e-3) / 1e9
+    alg_iter = 8.0 * E + 32.0 * V
+    iter_achieved = alg_iter * iters / (ms * 1e-3) / 1e9
+
+    line = {"metric": metric, "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" + ("(contrib f32)" if args.fp32_contrib else ""),
+            "data": "synthetic RMAT generated on device (sort_by_source%s)"
+                    % (", permuted ids" if args.permute else ", natural ids"),
+            "config": {"workload": workload, "V": V, "E": E, "iterations": iters,
+                       "schedule": SCHEDULES[args.schedule], "blocking_prep_ms": prep_ms,
+                       "generate_s": gen_s,
+                       "l2": "inputs (%.1f GB) larger than L2; no flush needed" % (8 * E / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "edge phase (%s)" % args.schedule,
+                         "avg_launch_ms": avg_edge_ms, "alg_bytes_per_launch": alg_edge,
+                         "iteration_frac": iter_achieved / peak},
+            "gpu_launches": launches,
+            "clocks": clk.summary()}
+
+    # e2e: host COO in pinned memory -> Graph.from_coo -> pagerank -> ranks on host
+    if not args.no_e2e:
+        src_h = torch.from_numpy(g.coo_src).pin_memory()
+        dst_h = torch.from_numpy(g.coo_dst).pin_memory()
+        g.close()
+        del g
+        torch.cuda.empty_cache()
+        ranks_h = torch.empty(V, dtype=torch.float64).pin_memory()
+        e2e_steps = min(2, args.steps)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ge = gg.Graph.from_coo(V, src_h.numpy(), dst_h.numpy(), device=local)
+            gg.pagerank(ge, prog, max_iters=iters, tolerance=0.0, out=ranks_h.numpy(),
+                        contrib_fp32=args.fp32_contrib)
+            ge.close()
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e_t = torch.tensor([e2e_s], device="cuda")
+        if dist is not None:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2e_t.item())
+        line["e2e"] = {"value": world * iters * E / e2e_s / 1e9, "unit": "GTEPS",
+                       "h2d_bytes_per_step": 8 * E, "d2h_bytes_per_step": 8 * V,
+                       "s_per_step": e2e_s,
+                       "includes": "H2D of COO from pinned host memory, device graph build "
+                                   "(EdgeBlocking prep), 20 iterations, D2H of ranks"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_pagerank_sample(min(args.cpu_scale, scale), ef, seed)
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,242 @@
+/* gg.h — C ABI of the B200-native edgeset.apply engine (libgg.so).
+ *
+ * This is the drop-in boundary for the reference's traversal hot path
+ * (package `schedge`, /root/reference/pkg/src/schedge).  The reference is a
+ * pure-Python package, so its "FFI" is the Python call surface; every entry
+ * point below names the reference interface it replaces (file:line, relative
+ * to /root/reference/pkg/src/schedge/).  The Python host package
+ * `paper_2012_07990_b200` binds these symbols with ctypes (see
+ * paper_2012_07990_b200/_lib.py and INTEGRATION.md).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no torch / C++ types cross the boundary;
+ *  - every function returns GG_OK (0) or a negative gg_status code, and the
+ *    message of the last failure on the calling thread is gg_last_error();
+ *  - "host or device" output pointers are written with cudaMemcpyDefault, so a
+ *    caller may pass either pinned/pageable host memory or a device pointer;
+ *  - a gg_graph is immutable after creation and may be shared by concurrent
+ *    queries on different host threads (graphio.py:19-26); a gg_runtime is
+ *    per query (algos.py:109, runtime.py:199-215).
+ */
+#ifndef GG_H
+#define GG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (error conventions of SURVEY §8b) -------------------- */
+typedef enum {
+  GG_OK = 0,
+  GG_ERR_SCHEDULE = -1, /* ScheduleError   sched.py:44, engine.py:434-436       */
+  GG_ERR_ENGINE = -2,   /* EngineError     runtime.py:58, engine.py:439-441     */
+  GG_ERR_VALUE = -3,    /* ValueError      algos.py:91-94, :222-224, :326-327   */
+  GG_ERR_CUDA = -4,     /* device failure (no reference analogue)               */
+  GG_ERR_NCCL = -5,     /* collective failure (no reference analogue)           */
+  GG_ERR_FRONTIER = -6, /* FrontierError   frontier.py:26                       */
+  GG_ERR_OOM = -7       /* device allocation failed                             */
+} gg_status;
+
+/* ---- schedule codes (sched.py:29-39 token order) ---------------------- */
+enum { GG_PUSH = 0, GG_PULL = 1 };
+enum { GG_SPARSE = 0, GG_BITMAP = 1, GG_BOOLMAP = 2 };
+enum {
+  GG_LB_VERTEX_BASED = 0, GG_LB_CM = 1, GG_LB_WM = 2, GG_LB_STRICT = 3,
+  GG_LB_EDGE_ONLY = 4, GG_LB_ETWC = 5, GG_LB_TWC = 6
+};
+enum { GG_CREATE_FUSED = 0, GG_CREATE_UNFUSED_BOOLMAP = 1, GG_CREATE_UNFUSED_BITMAP = 2 };
+enum { GG_DEDUP_MONOTONIC_COUNTERS = 0, GG_DEDUP_BITMAP = 1, GG_DEDUP_BOOLMAP = 2 };
+
+/* POD mirror of sched.Schedule (sched.py:55-71). blocking_size 0 = default. */
+typedef struct {
+  int32_t direction;
+  int32_t pull_repr;
+  int32_t load_balance;
+  int32_t blocking;
+  int64_t blocking_size;
+  int32_t frontier_creation;
+  int32_t dedup;
+  int32_t dedup_strategy;
+  int32_t kernel_fusion;
+  int64_t delta;
+} gg_schedule;
+
+/* A label binding: simple schedule or sched.HybridSchedule (sched.py:74-89). */
+typedef struct {
+  int32_t is_hybrid;
+  double threshold; /* resolved hybrid threshold in (0,1) */
+  gg_schedule s1;   /* the simple schedule when !is_hybrid */
+  gg_schedule s2;
+} gg_binding;
+
+/* Shape of the CTA hierarchy (runtime.ExecConfig, runtime.py:26-50).
+ * On the device cta_size is the block size used by the CTA-granular
+ * load balancers (ETWC stage-2 chunk, TWC CTA threshold); warp_size must be
+ * 32 there.  num_workers/deterministic are host-simulation knobs of the
+ * reference and only validated here. */
+typedef struct {
+  int32_t num_workers;
+  int32_t cta_size;
+  int32_t warp_size;
+  int32_t deterministic;
+} gg_exec;
+
+/* runtime.RunStats (runtime.py:53-67) + device timings. direction_log is a
+ * caller buffer of direction codes; direction_log_len reports the full
+ * length even when it exceeds direction_log_cap. */
+typedef struct {
+  int64_t dispatch_count;
+  int64_t rounds;
+  int64_t edges_traversed;
+  int64_t frontier_conversions;
+  int64_t frontier_allocations;
+  int64_t reused_frontiers;
+  int64_t creation_passes;
+  int32_t* direction_log;
+  int64_t direction_log_cap;
+  int64_t direction_log_len;
+  double kernel_ms;  /* device time of the algorithm (CUDA events) */
+  double wall_ms;    /* host wall time of the call */
+  int64_t gpu_launches; /* kernels this call launched */
+  double edge_ms;       /* device time of the edge-traversal phase (events)  */
+  int64_t edge_launches;/* number of edge-traversal phases timed in edge_ms */
+} gg_stats;
+
+typedef struct {
+  int32_t device;
+  int32_t sm_count;
+  int64_t l2_bytes;
+  int64_t hbm_bytes;
+  int32_t cc_major, cc_minor;
+  int32_t max_smem_per_block;
+  char name[128];
+} gg_device_info;
+
+typedef struct gg_graph gg_graph;       /* device-resident immutable graph   */
+typedef struct gg_runtime gg_runtime;   /* per-query state (stats, pools)    */
+typedef struct gg_frontier gg_frontier; /* device VertexSubset               */
+typedef struct gg_blocked gg_blocked;   /* device EdgeBlocking layout        */
+
+/* ---- library / device ---------------------------------------------------- */
+const char* gg_last_error(void);
+const char* gg_version(void);
+int gg_device_count(int32_t* count);
+int gg_device_info_get(int32_t device, gg_device_info* info);
+
+/* ---- graph (graphio.Graph.from_coo, graphio.py:58-81) ------------------------
+ * Builds CSR-out, CSR-in (CSC) and keeps the COO in load order, on `device`.
+ * CSR views are a stable counting sort of the COO (graphio.py:95-102), so
+ * neighbour order equals the reference's.  weights may be NULL.  Arrays are
+ * host pointers; gg_graph_create_device takes device pointers (copied). */
+int gg_graph_create(int32_t device, int64_t num_vertices, int64_t num_edges,
+                    const int32_t* src, const int32_t* dst, const uint32_t* weights,
+                    int32_t symmetric, gg_graph** out);
+int gg_graph_create_device(int32_t device, int64_t num_vertices, int64_t num_edges,
+                           const int32_t* d_src, const int32_t* d_dst,
+                           const uint32_t* d_weights, int32_t symmetric, gg_graph** out);
+int gg_graph_destroy(gg_graph* g);
+int gg_graph_info(const gg_graph* g, int64_t* num_vertices, int64_t* num_edges,
+                  int32_t* weighted, int32_t* symmetric, int32_t* device);
+/* which: 0 out_offsets(int64,V+1) 1 out_neighbors(int32,E) 2 out_weights(uint32,E)
+ *        3 in_offsets 4 in_neighbors 5 in_weights 6 coo_src 7 coo_dst 8 coo_weights */
+int gg_graph_copy_array(const gg_graph* g, int32_t which, void* out);
+/* Release the COO view (keeps CSR/CSC) to save HBM on the largest graphs. */
+int gg_graph_drop_coo(gg_graph* g);
+
+/* Synthetic inputs generated on the device (bench/test workloads, §8d).
+ *  kind 0: RMAT(scale, edge_factor, a, b, c) directed, duplicates + loops kept
+ *  kind 1: Graph500 Kronecker (same recursion, ids permuted)
+ *  kind 2: 2-D 4-neighbour grid side x side, arcs both ways
+ * flags: 1 = symmetrize+dedup (graphio._symmetrize semantics, graphio.py:118-140)
+ *        2 = permute vertex ids (seeded)   4 = attach uint32 weights U[1,1000]
+ *        8 = order the COO by source (edge-list-file order) */
+int gg_generate(int32_t device, int32_t kind, int32_t scale, int32_t edge_factor,
+                double a, double b, double c, uint64_t seed, int32_t flags,
+                gg_graph** out);
+
+/* ---- EdgeBlocking (blocking.py) ------------------------------------------ */
+/* default_blocking_size (blocking.py:63-66) but from the queried L2 size. */
+int64_t gg_default_blocking_size(const gg_graph* g);
+/* Alg. 1 on the device (blocking.py:78-113): stable partition of the COO by
+ * dst / n.  Cached on the graph per n (blocking.py:69-75). */
+int gg_block_edges(gg_graph* g, int64_t n, gg_blocked** out, double* prep_ms);
+int gg_blocked_info(const gg_blocked* b, int64_t* num_segments, int64_t* n);
+/* which: 0 segment_start(int64,S) 1 src(int32,E) 2 dst(int32,E) 3 weight(uint32,E) */
+int gg_blocked_copy_array(const gg_blocked* b, int32_t which, void* out);
+
+/* ---- runtime + frontier (runtime.py:160-248, frontier.py:129-269) ------- */
+int gg_runtime_create(const gg_graph* g, const gg_exec* cfg, gg_runtime** out);
+int gg_runtime_destroy(gg_runtime* rt);
+int gg_runtime_stats(gg_runtime* rt, gg_stats* out);
+/* FrontierPool.new_frontier (runtime.py:151-157): SPARSE subset of ids. */
+int gg_frontier_new(gg_runtime* rt, const int32_t* ids, int64_t n, gg_frontier** out);
+int gg_frontier_release(gg_runtime* rt, gg_frontier* f); /* FrontierPool.release */
+int gg_frontier_free(gg_frontier* f);
+int gg_frontier_size(gg_frontier* f, int64_t* size);      /* VertexSubset.size   */
+int gg_frontier_repr(const gg_frontier* f, int32_t* repr);
+/* VertexSubset.members (frontier.py:186-201): insertion order for SPARSE,
+ * ascending for dense.  out must hold `size` ids. */
+int gg_frontier_members(gg_frontier* f, int32_t* out, int64_t cap, int64_t* n);
+int gg_frontier_convert(gg_runtime* rt, gg_frontier* f, int32_t repr, gg_frontier** out);
+
+/* ---- edgeset.apply with a named device UDF (engine.py:418-460) ------------
+ * The reference accepts an arbitrary Python udf(ctx); on the device each udf
+ * is a named functor (SURVEY §7 hard part 1).  udf ids:
+ *   GG_UDF_BFS       state: int32 parent[V]        push CAS / pull store + enqueue,
+ *                                                   filter parent[v] == -1 (algos.py:114-125)
+ *   GG_UDF_COUNT     state: int64 counts[V]         atomic_add(counts[dst], 1)
+ *   GG_UDF_ENQUEUE   no state                       enqueue(dst)
+ *   GG_UDF_PR        state: double acc[V], contrib  atomic_add(acc[dst], contrib[src]) (algos.py:180-181)
+ * `filter` 0 = none, 1 = the udf's own filter.  device pointers in state. */
+enum { GG_UDF_BFS = 0, GG_UDF_COUNT = 1, GG_UDF_ENQUEUE = 2, GG_UDF_PR = 3 };
+typedef struct {
+  void* arr0;
+  void* arr1;
+  int64_t i0;
+} gg_udf_state;
+int gg_edgeset_apply(gg_runtime* rt, int32_t udf, const gg_udf_state* state, int32_t filter,
+                     gg_frontier* input /* NULL = all vertices */, const gg_binding* binding,
+                     int32_t reuse, int32_t collect_output, gg_frontier** out);
+
+/* ---- algorithm drivers (algos.py) ------------------------------------------
+ * fusion = the "s0" loop binding's kernel fusion (engine.fused_loop).  All
+ * outputs may be host or device pointers. */
+int gg_bfs(const gg_graph* g, int64_t source, const gg_binding* binding, int32_t fusion,
+           const gg_exec* cfg, int32_t* parents, gg_stats* stats);            /* algos.py:101 */
+int gg_pagerank(const gg_graph* g, const gg_binding* binding, int32_t fusion,
+                const gg_exec* cfg, int64_t max_iters, double tolerance, double damping,
+                double* ranks, gg_stats* stats);                              /* algos.py:163 */
+/* gg_pagerank with the contribution vector stored as f32 (accumulation stays
+ * f64); halves the bytes of the random gathers on the largest graphs. */
+int gg_pagerank_ex(const gg_graph* g, const gg_binding* binding, int32_t fusion,
+                   const gg_exec* cfg, int64_t max_iters, double tolerance, double damping,
+                   int32_t fp32_contrib, double* ranks, gg_stats* stats);
+int gg_sssp_delta(const gg_graph* g, int64_t source, const gg_binding* binding,
+                  int32_t fusion, const gg_exec* cfg, uint64_t* dist, gg_stats* stats); /* algos.py:215 */
+int gg_cc(const gg_graph* g, const gg_binding* binding, int32_t fusion, const gg_exec* cfg,
+          int32_t* labels, gg_stats* stats);                                  /* algos.py:267 */
+int gg_bc(const gg_graph* g, const int64_t* sources, int64_t num_sources,
+          const gg_binding* binding, const gg_exec* cfg, double* scores,
+          gg_stats* stats);                                                   /* algos.py:314 */
+
+/* ---- multi-GPU (1-D vertex partition, NCCL over NVLink) --------
+ * One process per GPU.  gg_nccl_unique_id fills 128 bytes on rank 0; the
+ * caller broadcasts it (torch.distributed) and every rank calls
+ * gg_comm_init.  gg_pagerank_dist runs PageRank on this rank's partition:
+ * the rank owns destinations [lo, hi) (balanced by in-edge count) and
+ * allgathers contributions every iteration. */
+typedef struct gg_comm gg_comm;
+int gg_nccl_unique_id(char out[128]);
+int gg_comm_init(int32_t device, int32_t nranks, int32_t rank, const char id[128],
+                 gg_comm** out);
+int gg_comm_destroy(gg_comm* c);
+int gg_pagerank_dist(gg_comm* c, const gg_graph* g, int64_t max_iters, double tolerance,
+                     double damping, double* ranks /* V, gathered on every rank */,
+                     gg_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GG_H */

@@ -1,0 +1,643 @@
+// engine.cu — edgeset.apply dispatcher, device frontiers and per-query runtime.
+//
+// Reference anchors (all in /root/reference/pkg/src/schedge/):
+//   edgeset_apply                  engine.py:418-460
+//   _apply_push/_apply_pull/_apply_edge_only   engine.py:463-608
+//   _OutputBuilder                 engine.py:279-397
+//   _sparse_view/_dense_view       engine.py:404-415
+//   hybrid_apply                   engine.py:622-636 (strictly greater)
+//   FrontierPool                   runtime.py:124-157
+//   VertexSubset.convert/members   frontier.py:186-265
+#include "engine.cuh"
+#include <cub/device/device_select.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+namespace gg {
+
+// ---------------------------------------------------------------------------
+// Frontier storage and conversions
+// ---------------------------------------------------------------------------
+std::unique_ptr<Frontier> frontier_alloc(int dev, int64_t universe, int repr, int64_t sparse_cap) {
+  auto f = std::make_unique<Frontier>();
+  f->dev = dev;
+  f->universe = universe;
+  f->repr = repr;
+  f->count.alloc(1);
+  f->count.zero();
+  if (repr == GG_SPARSE) {
+    f->ids.alloc(sparse_cap > 0 ? sparse_cap : 1);
+  } else if (repr == GG_BITMAP) {
+    f->bits.alloc((universe + 31) / 32 + 1);
+    f->bits.zero();
+  } else {
+    f->bools.alloc(((universe + 3) & ~int64_t(3)) + 4);
+    f->bools.zero();
+  }
+  f->size_cache = 0;
+  return f;
+}
+
+void frontier_clear(Frontier* f, cudaStream_t s) {
+  GG_CUDA(cudaMemsetAsync(f->count.p, 0, sizeof(unsigned long long), s));
+  if (f->repr == GG_BITMAP) f->bits.zero(s);
+  if (f->repr == GG_BOOLMAP) f->bools.zero(s);
+  f->size_cache = 0;
+}
+
+__global__ void k_popcount_bits(const uint32_t* w, int64_t nwords, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwords;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += __popc(w[i]);
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+__global__ void k_popcount_bytes(const uint8_t* b, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += b[i] != 0;
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+// dense size into f->count (the unfused "separate materialisation pass")
+static void dense_size_on_device(Frontier* f, cudaStream_t s) {
+  GG_CUDA(cudaMemsetAsync(f->count.p, 0, sizeof(unsigned long long), s));
+  if (f->repr == GG_BITMAP) {
+    int64_t nw = (f->universe + 31) / 32;
+    k_popcount_bits<<<grid_for(nw, 256, f->dev), 256, 0, s>>>(f->bits.p, nw, f->count.p);
+  } else {
+    k_popcount_bytes<<<grid_for(f->universe, 256, f->dev), 256, 0, s>>>(f->bools.p, f->universe,
+                                                                         f->count.p);
+  }
+  GG_LAUNCH_CHECK();
+  count_launch();
+  f->size_cache = -1;
+}
+
+int64_t frontier_size_raw(Frontier* f, cudaStream_t s) {
+  if (f->size_cache >= 0) return f->size_cache;
+  unsigned long long h = 0;
+  GG_CUDA(cudaMemcpyAsync(&h, f->count.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GG_CUDA(cudaStreamSynchronize(s));
+  f->size_cache = (int64_t)h;
+  return f->size_cache;
+}
+
+int64_t frontier_size(Runtime* rt, Frontier* f) { return frontier_size_raw(f, rt->stream); }
+
+struct MemberPred {
+  const uint32_t* bits;
+  const uint8_t* bools;
+  __device__ __forceinline__ bool operator()(int32_t v) const {
+    return bits ? ((bits[v >> 5] >> (v & 31)) & 1u) : (bools[v] != 0);
+  }
+};
+
+__global__ void k_sparse_to_bits(const int32_t* ids, const unsigned long long* n, uint32_t* bits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = ids[i];
+    atomicOr(bits + (v >> 5), 1u << (v & 31));
+  }
+}
+__global__ void k_sparse_to_bytes(const int32_t* ids, const unsigned long long* n, uint8_t* b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[ids[i]] = 1;
+}
+__global__ void k_bits_to_bytes(const uint32_t* bits, int64_t V, uint8_t* b) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    b[v] = (bits[v >> 5] >> (v & 31)) & 1u;
+}
+__global__ void k_bytes_to_bits(const uint8_t* b, int64_t V, uint32_t* bits) {
+  // one warp builds one word: ballot over 32 consecutive bytes
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); base < V;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = base + lane_id();
+    unsigned m = __ballot_sync(0xffffffffu, v < V && b[v] != 0);
+    if (lane_id() == 0) bits[base >> 5] = m;
+  }
+}
+
+void frontier_convert_into(Runtime* rt, Frontier* src, Frontier* dst) {
+  cudaStream_t s = rt->stream;
+  const int dev = rt->dev;
+  frontier_clear(dst, s);
+  const int64_t V = src->universe;
+  if (src->repr == dst->repr) {
+    if (src->repr == GG_SPARSE) {
+      int64_t n = frontier_size_raw(src, s);
+      if (n) GG_CUDA(cudaMemcpyAsync(dst->ids.p, src->ids.p, n * 4, cudaMemcpyDeviceToDevice, s));
+    } else if (src->repr == GG_BITMAP) {
+      GG_CUDA(cudaMemcpyAsync(dst->bits.p, src->bits.p, src->bits.bytes(), cudaMemcpyDeviceToDevice, s));
+    } else {
+      GG_CUDA(cudaMemcpyAsync(dst->bools.p, src->bools.p, src->bools.bytes(), cudaMemcpyDeviceToDevice, s));
+    }
+    GG_CUDA(cudaMemcpyAsync(dst->count.p, src->count.p, 8, cudaMemcpyDeviceToDevice, s));
+    dst->size_cache = src->size_cache;
+    return;
+  }
+  if (dst->repr == GG_SPARSE) {
+    // dense -> SPARSE in ascending id order (frontier.py:186-201)
+    MemberPred pred{src->repr == GG_BITMAP ? src->bits.p : nullptr,
+                    src->repr == GG_BOOLMAP ? src->bools.p : nullptr};
+    cub::CountingInputIterator<int32_t> it(0);
+    size_t temp = 0;
+    GG_CUDA(cub::DeviceSelect::If(nullptr, temp, it, dst->ids.p, dst->count.p, V, pred, s));
+    GG_CUDA(cub::DeviceSelect::If(rt->cub_tmp.get(temp), temp, it, dst->ids.p, dst->count.p, V, pred, s));
+    count_launch();
+    dst->size_cache = -1;
+    return;
+  }
+  if (src->repr == GG_SPARSE) {
+    // sparse -> dense deduplicates by construction
+    if (dst->repr == GG_BITMAP)
+      k_sparse_to_bits<<<grid_for(V, 256, dev), 256, 0, s>>>(src->ids.p, src->count.p, dst->bits.p);
+    else
+      k_sparse_to_bytes<<<grid_for(V, 256, dev), 256, 0, s>>>(src->ids.p, src->count.p, dst->bools.p);
+  } else if (dst->repr == GG_BOOLMAP) {
+    k_bits_to_bytes<<<grid_for(V, 256, dev), 256, 0, s>>>(src->bits.p, V, dst->bools.p);
+  } else {
+    k_bytes_to_bits<<<grid_for(V, 256, dev), 256, 0, s>>>(src->bools.p, V, dst->bits.p);
+  }
+  GG_LAUNCH_CHECK();
+  count_launch();
+  dense_size_on_device(dst, s);
+}
+
+void frontier_members(Frontier* f, int32_t* out, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  if (f->repr == GG_SPARSE) {
+    GG_CUDA(cudaMemcpyAsync(out, f->ids.p, n * 4, cudaMemcpyDefault, s));
+    GG_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  Frontier tmp;
+  tmp.dev = f->dev;
+  tmp.universe = f->universe;
+  tmp.repr = GG_SPARSE;
+  tmp.ids.alloc(f->universe);
+  tmp.count.alloc(1);
+  MemberPred pred{f->repr == GG_BITMAP ? f->bits.p : nullptr,
+                  f->repr == GG_BOOLMAP ? f->bools.p : nullptr};
+  cub::CountingInputIterator<int32_t> it(0);
+  size_t temp = 0;
+  GG_CUDA(cub::DeviceSelect::If(nullptr, temp, it, tmp.ids.p, tmp.count.p, f->universe, pred, s));
+  DevBuf<uint8_t> tb(temp);
+  GG_CUDA(cub::DeviceSelect::If(tb.p, temp, it, tmp.ids.p, tmp.count.p, f->universe, pred, s));
+  GG_CUDA(cudaMemcpyAsync(out, tmp.ids.p, n * 4, cudaMemcpyDefault, s));
+  GG_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
+// Runtime
+// ---------------------------------------------------------------------------
+Runtime::Runtime(const Graph* graph, const gg_exec* c) : g(graph), dev(graph->dev) {
+  if (c) cfg = *c;
+  if (cfg.num_workers < 1) fail(GG_ERR_ENGINE, "num_workers must be >= 1");
+  if (cfg.warp_size < 1 || cfg.cta_size < 1) fail(GG_ERR_ENGINE, "warp_size and cta_size must be >= 1");
+  if (cfg.cta_size % cfg.warp_size) fail(GG_ERR_ENGINE, "warp_size must divide cta_size");
+  scanned.alloc(1);
+  scanned.zero();
+}
+
+Runtime::~Runtime() {
+  for (auto& p : edge_events) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  if (edge_open) cudaEventDestroy(edge_open);
+}
+
+void Runtime::edge_begin() {
+  GG_CUDA(cudaEventCreate(&edge_open));
+  GG_CUDA(cudaEventRecord(edge_open, stream));
+}
+
+void Runtime::edge_end() {
+  cudaEvent_t e;
+  GG_CUDA(cudaEventCreate(&e));
+  GG_CUDA(cudaEventRecord(e, stream));
+  edge_events.emplace_back(edge_open, e);
+  edge_open = nullptr;
+}
+
+double Runtime::edge_ms(int64_t* launches) {
+  double total = 0;
+  for (auto& p : edge_events) {
+    GG_CUDA(cudaEventSynchronize(p.second));
+    float ms = 0;
+    GG_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+    total += ms;
+  }
+  if (launches) *launches = (int64_t)edge_events.size();
+  return total;
+}
+
+int64_t Runtime::edges_traversed() {
+  unsigned long long h = 0;
+  GG_CUDA(cudaMemcpyAsync(&h, scanned.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
+  GG_CUDA(cudaStreamSynchronize(stream));
+  return stats.edges_traversed + (int64_t)h;
+}
+
+static int64_t sparse_capacity(const Graph* g) {
+  // A SPARSE frontier with dedup off may hold one entry per scanned arc.
+  return std::max<int64_t>(g->V, g->E) + 1;
+}
+
+std::unique_ptr<Frontier> Runtime::acquire(int repr) {
+  if (spare[repr]) {
+    auto f = std::move(spare[repr]);
+    f->retired = false;
+    return f;
+  }
+  stats.frontier_allocations += 1;
+  return frontier_alloc(dev, g->V, repr, repr == GG_SPARSE ? sparse_capacity(g) : 0);
+}
+
+void Runtime::release(std::unique_ptr<Frontier> f) {
+  if (!f) return;
+  frontier_clear(f.get(), stream);
+  f->retired = true;
+  if (!spare[f->repr]) spare[f->repr] = std::move(f);
+}
+
+__global__ void k_check_ids(const int32_t* ids, int64_t n, int64_t V, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (ids[i] < 0 || ids[i] >= V) *bad = 1;
+}
+
+std::unique_ptr<Frontier> Runtime::new_frontier(const int32_t* ids, int64_t n) {
+  auto f = acquire(GG_SPARSE);
+  if (n > (int64_t)f->ids.n) fail(GG_ERR_ENGINE, "frontier larger than its capacity");
+  if (n) {
+    GG_CUDA(cudaMemcpyAsync(f->ids.p, ids, n * 4, cudaMemcpyDefault, stream));
+    DevBuf<int> bad(1);
+    bad.zero(stream);
+    k_check_ids<<<grid_for(n, 256, dev), 256, 0, stream>>>(f->ids.p, n, g->V, bad.p);
+    GG_LAUNCH_CHECK();
+    int hb = 0;
+    GG_CUDA(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, stream));
+    GG_CUDA(cudaStreamSynchronize(stream));
+    if (hb) fail(GG_ERR_ENGINE, "vertex id out of range");
+  }
+  unsigned long long hn = (unsigned long long)n;
+  GG_CUDA(cudaMemcpyAsync(f->count.p, &hn, 8, cudaMemcpyHostToDevice, stream));
+  GG_CUDA(cudaStreamSynchronize(stream));
+  f->size_cache = n;
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// Schedule validation (sched.py:123-153)
+// ---------------------------------------------------------------------------
+void check_schedule(const gg_schedule& s) {
+  std::string p;
+  auto add = [&](const char* m) { p += p.empty() ? m : (std::string("; ") + m); };
+  if (s.direction != GG_PUSH && s.direction != GG_PULL) add("unknown direction");
+  if (s.pull_repr != GG_BOOLMAP && s.pull_repr != GG_BITMAP) add("unknown pull frontier representation");
+  if (s.load_balance < 0 || s.load_balance > 6) add("unknown load balance");
+  if (s.frontier_creation < 0 || s.frontier_creation > 2) add("unknown frontier creation");
+  if (s.dedup_strategy < 0 || s.dedup_strategy > 2) add("unknown dedup strategy");
+  if (s.blocking && s.load_balance != GG_LB_EDGE_ONLY) add("blocking requires EDGE_ONLY load balancing");
+  if (s.blocking_size < 0) add("blocking_size must be >= 1");
+  if (s.delta < 1) add("delta must be >= 1");
+  if (!p.empty()) fail(GG_ERR_SCHEDULE, "invalid schedule: " + p);
+}
+
+void check_binding(const gg_binding& b) {
+  check_schedule(b.s1);
+  if (b.is_hybrid) {
+    check_schedule(b.s2);
+    if (!(b.threshold > 0.0 && b.threshold < 1.0)) fail(GG_ERR_SCHEDULE, "threshold must lie in (0, 1)");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dispatch
+// ---------------------------------------------------------------------------
+static int max_coop_blocks(const void* fn, int block, int dev, size_t smem = 0) {
+  int per_sm = 0;
+  GG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+  if (per_sm < 1) fail(GG_ERR_CUDA, "kernel cannot be co-resident");
+  return per_sm * sm_count(dev);
+}
+
+__global__ void k_degrees_of(const InView in, const int64_t* off, int64_t n, int64_t* deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { deg[i] = 0; continue; }
+    int32_t u = active_at(in, i);
+    deg[i] = off[u + 1] - off[u];
+  }
+}
+
+__global__ void k_strict_spans(const int64_t* off, int64_t V, int64_t nspans, int64_t* span) {
+  const int64_t total = off[V];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= nspans;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t == nspans) { span[t] = V; continue; }
+    // edge target of span t, snapped to the first vertex whose range starts
+    // at or after it (bisect_left over offsets, engine.py:216-225)
+    int64_t target = (int64_t)((__int128)total * t / nspans);
+    int64_t lo = 0, hi = V;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (off[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    span[t] = t == 0 ? 0 : lo;
+  }
+}
+
+__global__ void k_clear_marks(const int32_t* ids, const unsigned long long* n, uint32_t* bits,
+                              uint8_t* bytes) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = ids[i];
+    if (bits) atomicAnd(bits + (v >> 5), ~(1u << (v & 31)));
+    if (bytes) bytes[v] = 0;
+  }
+}
+
+template <class Op>
+static void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
+                     int64_t n_host, const OutBuilder& out) {
+  const Graph* g = rt->g;
+  cudaStream_t st = rt->stream;
+  PushArgs<Op> a{g->out_view(), in, op, out, use_filter ? 1 : 0, rt->scanned.p};
+  const int dev = rt->dev;
+  const int64_t work = n_host >= 0 ? n_host : g->V;
+  const int cta = rt->cfg.cta_size;
+  switch (s.load_balance) {
+    case GG_LB_VERTEX_BASED:
+      k_push_vb<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_WM:
+      k_push_wm<Op><<<grid_for(work * 8, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_CM:
+      k_push_cm<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_ETWC:
+      k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
+      break;
+    case GG_LB_STRICT: {
+      const int64_t n = n_host >= 0 ? n_host : g->V;
+      rt->prefix.alloc(n + 1);
+      DevBuf<int64_t> deg(n + 1);
+      k_degrees_of<<<grid_for(n + 1, 256, dev), 256, 0, st>>>(in, g->out_off.p, n, deg.p);
+      GG_LAUNCH_CHECK();
+      size_t temp = 0;
+      GG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, deg.p, rt->prefix.p, n + 1, st));
+      GG_CUDA(cub::DeviceScan::ExclusiveSum(rt->cub_tmp.get(temp), temp, deg.p, rt->prefix.p, n + 1, st));
+      count_launch(2);
+      k_push_strict<Op><<<grid_for(g->E / 32 + 1, 256, dev), 256, 0, st>>>(a, rt->prefix.p, 32);
+      GG_CUDA(cudaStreamSynchronize(st));  // deg freed at scope end
+      break;
+    }
+    case GG_LB_TWC: {
+      if (rt->twc_q.n < (size_t)(3 * g->V + 3)) rt->twc_q.alloc(3 * g->V + 3);
+      if (!rt->twc_cnt.p) rt->twc_cnt.alloc(3);
+      GG_CUDA(cudaMemsetAsync(rt->twc_cnt.p, 0, 3 * 8, st));
+      TwcQueues q{{rt->twc_q.p, rt->twc_q.p + g->V + 1, rt->twc_q.p + 2 * (g->V + 1)}, rt->twc_cnt.p};
+      k_twc_bin<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q, cta);
+      a.scanned = rt->scanned.p;
+      k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
+      k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
+      k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      count_launch(3);
+      break;
+    }
+    default:
+      fail(GG_ERR_ENGINE, "no chunker for this load balance");
+  }
+  GG_LAUNCH_CHECK();
+  count_launch();
+}
+
+template <class Op>
+static void run_pull(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
+                     const OutBuilder& out) {
+  const Graph* g = rt->g;
+  cudaStream_t st = rt->stream;
+  PullArgs<Op> a{g->in_view(), in, op, out, use_filter ? 1 : 0, rt->scanned.p};
+  const int dev = rt->dev;
+  const int64_t V = g->V;
+  const int cta = rt->cfg.cta_size;
+  switch (s.load_balance) {
+    case GG_LB_VERTEX_BASED:
+      k_pull_vb<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_WM:
+      k_pull_wm<Op><<<grid_for(V * 32, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_CM:
+      k_pull_cm<Op><<<grid_for(V * 256, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_ETWC:
+      k_pull_etwc<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, cta);
+      break;
+    case GG_LB_STRICT: {
+      const int64_t nspans = std::min<int64_t>(V > 0 ? V : 1, (int64_t)sm_count(dev) * 2048);
+      if (rt->spans_n != nspans) {
+        rt->spans.alloc(nspans + 1);
+        k_strict_spans<<<grid_for(nspans + 1, 256, dev), 256, 0, st>>>(g->in_off.p, V, nspans,
+                                                                         rt->spans.p);
+        GG_LAUNCH_CHECK();
+        count_launch();
+        rt->spans_n = nspans;
+      }
+      k_pull_strict<Op><<<grid_for(nspans, 256, dev), 256, 0, st>>>(a, rt->spans.p, nspans);
+      break;
+    }
+    case GG_LB_TWC: {
+      if (rt->twc_q.n < (size_t)(3 * V + 3)) rt->twc_q.alloc(3 * V + 3);
+      if (!rt->twc_cnt.p) rt->twc_cnt.alloc(3);
+      GG_CUDA(cudaMemsetAsync(rt->twc_cnt.p, 0, 3 * 8, st));
+      TwcQueues q{{rt->twc_q.p, rt->twc_q.p + V + 1, rt->twc_q.p + 2 * (V + 1)}, rt->twc_cnt.p};
+      k_pull_twc_bin<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, q, cta);
+      k_pull_twc_thread<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
+      k_pull_twc_warp<Op><<<grid_for(V * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
+      k_pull_twc_cta<Op><<<grid_for(V * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      count_launch(3);
+      break;
+    }
+    default:
+      fail(GG_ERR_ENGINE, "no pull partitioner for this load balance");
+  }
+  GG_LAUNCH_CHECK();
+  count_launch();
+}
+
+template <class Op>
+static void run_edge_only(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
+                          const OutBuilder& out) {
+  const Graph* g = rt->g;
+  cudaStream_t st = rt->stream;
+  const int dev = rt->dev;
+  if (!g->has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
+  EdgeArgs<Op> a{g->coo_view(), in, op, out, use_filter ? 1 : 0};
+  if (s.blocking) {
+    int64_t n = s.blocking_size > 0 ? s.blocking_size : default_blocking_size(*g);
+    Blocked* b = blocked_for(*const_cast<Graph*>(g), n);
+    a.coo = CooView{b->src.p, b->dst.p, g->weighted ? b->w.p : nullptr, b->E};
+    const int64_t* seg = b->seg_end.p;
+    int64_t nseg = b->nseg;
+    void* args[] = {&a, &seg, &nseg};
+    int blocks = max_coop_blocks((const void*)k_edge_blocked<Op>, 256, dev);
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_edge_blocked<Op>, blocks, 256, args, 0, st));
+  } else {
+    k_edge_only<Op><<<grid_for(g->E / 4 + 1, 256, dev, 16), 256, 0, st>>>(a);
+    GG_LAUNCH_CHECK();
+  }
+  count_launch();
+  rt->stats.edges_traversed += g->E;
+}
+
+// The output builder configuration of _OutputBuilder.__init__ (engine.py:288-309).
+static OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out) {
+  OutBuilder ob{};
+  ob.mode = out ? s.frontier_creation : OUT_NONE;
+  ob.dedup = DEDUP_NONE;
+  if (!out) return ob;
+  ob.queue = out->ids.p;
+  ob.qcount = out->count.p;
+  ob.bits = out->bits.p;
+  ob.bools = out->bools.p;
+  const int64_t V = rt->g->V;
+  if (s.dedup) {
+    if (s.dedup_strategy == GG_DEDUP_MONOTONIC_COUNTERS) {
+      if (!rt->stamps.p) {
+        rt->stamps.alloc(V + 1);
+        GG_CUDA(cudaMemsetAsync(rt->stamps.p, 0xff, rt->stamps.bytes(), rt->stream));
+      }
+      rt->round += 1;  // counters.next_round()
+      ob.dedup = DEDUP_COUNTERS;
+      ob.stamps = rt->stamps.p;
+      ob.round = rt->round;
+    } else if (s.frontier_creation == GG_CREATE_FUSED) {
+      if (s.dedup_strategy == GG_DEDUP_BITMAP) {
+        if (!rt->mark_bits.p) { rt->mark_bits.alloc((V + 31) / 32 + 1); rt->mark_bits.zero(rt->stream); }
+        ob.dedup = DEDUP_MARK_BITS;
+        ob.mark_bits = rt->mark_bits.p;
+      } else {
+        if (!rt->mark_bytes.p) { rt->mark_bytes.alloc(((V + 3) & ~int64_t(3)) + 4); rt->mark_bytes.zero(rt->stream); }
+        ob.dedup = DEDUP_MARK_BYTES;
+        ob.mark_bytes = rt->mark_bytes.p;
+      }
+    } else {
+      ob.dedup = DEDUP_SLOT;
+    }
+  }
+  return ob;
+}
+
+template <class Op>
+static std::unique_ptr<Frontier> apply_op(Runtime* rt, const Op& op, bool use_filter,
+                                          std::unique_ptr<Frontier>* input, const gg_binding& b,
+                                          bool reuse, bool collect_output) {
+  check_binding(b);
+  const Graph* g = rt->g;
+  Frontier* in = input ? input->get() : nullptr;
+  if (in && in->universe != g->V)
+    fail(GG_ERR_ENGINE, strf("frontier universe %lld does not match graph (%lld vertices)",
+                             (long long)in->universe, (long long)g->V));
+  if (in && in->retired) fail(GG_ERR_FRONTIER, "frontier was retired");
+  // hybrid_apply: s2 iff |input| > threshold * |V| (engine.py:631-632)
+  const gg_schedule* sp = &b.s1;
+  if (b.is_hybrid) {
+    int64_t size = in ? frontier_size(rt, in) : 0;
+    sp = ((double)size > b.threshold * (double)g->V) ? &b.s2 : &b.s1;
+  }
+  const gg_schedule& s = *sp;
+  rt->stats.direction_log.push_back(s.direction);
+
+  std::unique_ptr<Frontier> out;
+  if (collect_output) {
+    int repr = s.frontier_creation == GG_CREATE_FUSED
+                   ? GG_SPARSE
+                   : (s.frontier_creation == GG_CREATE_UNFUSED_BOOLMAP ? GG_BOOLMAP : GG_BITMAP);
+    out = rt->acquire(repr);
+    frontier_clear(out.get(), rt->stream);
+  }
+  OutBuilder ob = make_builder(rt, s, out.get());
+
+  // input views (engine.py:404-415, 559-565)
+  auto converted = [&](int repr) -> Frontier* {
+    rt->stats.frontier_conversions += 1;
+    if (!rt->conv || rt->conv->repr != repr)
+      rt->conv = frontier_alloc(rt->dev, g->V, repr, repr == GG_SPARSE ? sparse_capacity(g) : 0);
+    frontier_convert_into(rt, in, rt->conv.get());
+    return rt->conv.get();
+  };
+  InView iv{};
+  iv.repr = -1;
+  if (s.load_balance == GG_LB_EDGE_ONLY) {
+    if (in) iv = (in->repr == GG_SPARSE ? converted(GG_BOOLMAP) : in)->view();
+    run_edge_only(rt, s, op, use_filter, iv, ob);
+  } else if (s.direction == GG_PUSH) {
+    int64_t n_host = g->V;
+    if (in) {
+      Frontier* sv = in->repr == GG_SPARSE ? in : converted(GG_SPARSE);
+      iv = sv->view();
+      n_host = frontier_size_raw(sv, rt->stream);
+    }
+    if (n_host > 0) run_push(rt, s, op, use_filter, iv, n_host, ob);
+  } else {
+    if (in) iv = (in->repr == s.pull_repr ? in : converted(s.pull_repr))->view();
+    run_pull(rt, s, op, use_filter, iv, ob);
+  }
+  if (rt->fused_depth == 0) rt->stats.dispatch_count += 1;
+
+  // finalize (engine.py:383-397)
+  if (out) {
+    if (s.frontier_creation == GG_CREATE_FUSED) {
+      if (ob.dedup == DEDUP_MARK_BITS || ob.dedup == DEDUP_MARK_BYTES) {
+        k_clear_marks<<<grid_for(g->V, 256, rt->dev), 256, 0, rt->stream>>>(
+            out->ids.p, out->count.p, ob.mark_bits, ob.mark_bytes);
+        GG_LAUNCH_CHECK();
+        count_launch();
+      }
+      out->size_cache = -1;
+    } else {
+      dense_size_on_device(out.get(), rt->stream);
+      rt->stats.creation_passes += 1;
+    }
+  }
+  if (reuse && input && *input) {
+    rt->release(std::move(*input));
+    rt->stats.reused_frontiers += 1;
+  }
+  return out;
+}
+
+std::unique_ptr<Frontier> edgeset_apply(Runtime* rt, int udf, const gg_udf_state& st, bool use_filter,
+                                        std::unique_ptr<Frontier>* input, const gg_binding& b,
+                                        bool reuse, bool collect_output) {
+  DeviceGuard guard(rt->dev);
+  switch (udf) {
+    case UDF_BFS:
+      return apply_op(rt, OpBfs{(int32_t*)st.arr0}, use_filter, input, b, reuse, collect_output);
+    case UDF_COUNT:
+      return apply_op(rt, OpCount{(unsigned long long*)st.arr0}, use_filter, input, b, reuse,
+                      collect_output);
+    case UDF_ENQUEUE:
+      return apply_op(rt, OpEnqueue{}, use_filter, input, b, reuse, collect_output);
+    case UDF_PR:
+      return apply_op(rt, OpPr<double>{(double*)st.arr0, (const double*)st.arr1}, use_filter, input,
+                      b, reuse, collect_output);
+    case UDF_PR32:
+      return apply_op(rt, OpPr<float>{(double*)st.arr0, (const float*)st.arr1}, use_filter, input, b,
+                      reuse, collect_output);
+    default:
+      fail(GG_ERR_VALUE, "unknown udf id");
+  }
+}
+
+}  // namespace gg

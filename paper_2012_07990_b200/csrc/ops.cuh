@@ -1,0 +1,107 @@
+// ops.cuh — named device UDFs.  The reference runs an arbitrary Python
+// callable per edge through EdgeContext (runtime.py:299-362); a GPU cannot,
+// so every UDF the reference's algorithms and tests use is a functor here
+// (SURVEY §7 hard part 1).  Each functor provides
+//   filter(v)                       to_filter of the algorithm
+//   push(u, v, w, out)              atomic interface (PUSH / EDGE_ONLY)
+//   Acc init / visit / combine / finish   owner-write interface (PULL)
+#pragma once
+#include "traverse.cuh"
+
+namespace gg {
+
+template <class T>
+__device__ __forceinline__ T shfl_xor_any(T v, int o) {
+  return __shfl_xor_sync(0xffffffffu, v, o);
+}
+
+// BFS (algos.py:114-125): parent CAS in push; plain owner store in pull.
+struct OpBfs {
+  int32_t* parent;
+  using Acc = int32_t;
+  static constexpr bool kEarlyExit = true;
+  __device__ __forceinline__ bool filter(int32_t v) const {
+    return *((volatile int32_t*)parent + v) == -1;
+  }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder& out) const {
+    if (atomicCAS(parent + v, -1, u) == -1) out.emit(v);
+  }
+  __device__ __forceinline__ Acc init() const { return -1; }
+  __device__ __forceinline__ bool visit(Acc& acc, int32_t u, uint32_t) const {
+    if (acc == -1) acc = u;
+    return true;  // the first frontier in-neighbour settles v (algos.py:121-125)
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return a != -1 ? a : b; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = combine(a, shfl_xor_any(a, o));
+    return a;
+  }
+  __device__ __forceinline__ void finish(int32_t v, const Acc& acc, const OutBuilder& out) const {
+    if (acc != -1 && parent[v] == -1) {
+      parent[v] = acc;
+      out.emit(v);
+    }
+  }
+};
+
+// Test UDF: in-degree counting from the active set (test_engine.py:246-264).
+struct OpCount {
+  unsigned long long* counts;
+  using Acc = unsigned long long;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ void push(int32_t, int32_t v, uint32_t, const OutBuilder&) const {
+    atomicAdd(counts + v, 1ULL);
+  }
+  __device__ __forceinline__ Acc init() const { return 0; }
+  __device__ __forceinline__ bool visit(Acc& acc, int32_t, uint32_t) const { ++acc; return false; }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return a + b; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return warp_sum(a); }
+  __device__ __forceinline__ void finish(int32_t v, const Acc& acc, const OutBuilder&) const {
+    if (acc) counts[v] += acc;
+  }
+};
+
+// Test UDF: ctx.enqueue(ctx.dst) with no guard (test_engine.py:384-399);
+// pull enqueues once per member in-edge, like the reference's owner loop.
+struct OpEnqueue {
+  using Acc = unsigned long long;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ void push(int32_t, int32_t v, uint32_t, const OutBuilder& out) const {
+    out.emit(v);
+  }
+  __device__ __forceinline__ Acc init() const { return 0; }
+  __device__ __forceinline__ bool visit(Acc& acc, int32_t, uint32_t) const { ++acc; return false; }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return a + b; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return warp_sum(a); }
+  __device__ __forceinline__ void finish(int32_t v, const Acc& acc, const OutBuilder& out) const {
+    for (unsigned long long k = 0; k < acc; ++k) out.emit(v);
+  }
+};
+
+// PageRank gather (algos.py:180-181): acc[dst] += contrib[src].
+template <class CT>
+struct OpPr {
+  double* acc;
+  const CT* contrib;
+  using Acc = double;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
+    atomicAdd(acc + v, (double)__ldg(contrib + u));
+  }
+  __device__ __forceinline__ Acc init() const { return 0.0; }
+  __device__ __forceinline__ bool visit(Acc& a, int32_t u, uint32_t) const {
+    a += (double)__ldg(contrib + u);
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return a + b; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return warp_sum(a); }
+  __device__ __forceinline__ void finish(int32_t v, const Acc& a, const OutBuilder&) const {
+    if (a != 0.0) acc[v] += a;
+  }
+};
+
+}  // namespace gg

@@ -1,0 +1,251 @@
+// pagerank.cu — algos.pagerank (reference algos.py:163-208) on the device.
+//
+// Per iteration (reference semantics):
+//   dm      = sum(rank[v] for out_deg(v) == 0)         (pre-update rank)
+//   contrib = rank / out_deg (0 for dangling)
+//   acc[dst] += contrib[src]  over the schedule's edge traversal
+//   rank'   = (1-d)/n + d*dm/n + d*acc ;  l1 = sum|rank' - rank| ; acc = 0
+// The stop test runs before each body with l1 = inf initially
+// (algos.py:178, 204-205), so tolerance <= 0 gives exactly max_iters rounds.
+//
+// Device layout: rank f64[V], acc f64[V], contrib CT[V] (CT = f64, or f32
+// when requested), per-iteration scalars f64[2*(iters+1)] (dm, l1) so that
+// no host synchronisation is needed between rounds unless tolerance > 0.
+// The vertex pass fuses: rank update, L1, next dangling mass, next contrib
+// and the acc reset (one read of acc/rank/deg, one write of rank/contrib/acc).
+#include "engine.cuh"
+
+namespace gg {
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double s[32];
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane_id() == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < (blockDim.x >> 5) ? s[threadIdx.x] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+template <class CT>
+__global__ void __launch_bounds__(256) k_pr_init(const int64_t* off, int64_t V, double* rank,
+                                                 CT* contrib, double* acc, double* dm0) {
+  const double r0 = 1.0 / (double)V;
+  double dm = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = off[v + 1] - off[v];
+    rank[v] = r0;
+    acc[v] = 0.0;
+    contrib[v] = d ? (CT)(r0 / (double)d) : (CT)0;
+    if (!d) dm += r0;
+  }
+  dm = block_sum(dm);
+  if (threadIdx.x == 0 && dm != 0.0) atomicAdd(dm0, dm);
+}
+
+// Vertex pass of iteration `it` (algos.py:192-198 fused with :184-189 of it+1).
+template <class CT>
+__device__ __forceinline__ void pr_update_range(const int64_t* off, int64_t V, double* rank,
+                                                CT* contrib, double* acc, double* scal, int64_t it,
+                                                double damping, int64_t v0, int64_t stride) {
+  const double n = (double)V;
+  const double base = (1.0 - damping) / n + damping * scal[2 * it] / n;
+  double l1 = 0, dm = 0;
+  for (int64_t v = v0; v < V; v += stride) {
+    int64_t d = __ldg(off + v + 1) - __ldg(off + v);
+    double nv = base + damping * acc[v];
+    l1 += fabs(nv - rank[v]);
+    rank[v] = nv;
+    acc[v] = 0.0;
+    if (d) contrib[v] = (CT)(nv / (double)d);
+    else dm += nv;
+  }
+  l1 = block_sum(l1);
+  dm = block_sum(dm);
+  if (threadIdx.x == 0) {
+    if (l1 != 0.0) atomicAdd(scal + 2 * it + 1, l1);
+    if (dm != 0.0) atomicAdd(scal + 2 * (it + 1), dm);
+  }
+}
+
+template <class CT>
+__global__ void __launch_bounds__(256) k_pr_update(const int64_t* off, int64_t V, double* rank,
+                                                   CT* contrib, double* acc, double* scal,
+                                                   int64_t it, double damping) {
+  pr_update_range(off, V, rank, contrib, acc, scal, it, damping,
+                  blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// Fused loop (engine.fused_loop with fusion=True, engine.py:639-662): the
+// whole while-loop is one cooperative launch; rounds are separated by grid
+// barriers and the stop test is evaluated on the device.
+// Edge phase: EDGE_ONLY (flat, or blocked with a barrier per segment), PULL
+// (thread per destination, register accumulation) or PUSH (thread per source).
+// ---------------------------------------------------------------------------
+template <class CT>
+struct PrFusedArgs {
+  CsrView out, in;
+  CooView coo;
+  const int64_t* seg_end;
+  int64_t nseg;
+  int mode;  // 0 edge-only, 1 blocked, 2 pull, 3 push
+  double* rank;
+  CT* contrib;
+  double* acc;
+  double* scal;
+  int64_t max_iters;
+  double tol, damping;
+  int64_t* iters_out;
+};
+
+template <class CT>
+__global__ void __launch_bounds__(256) k_pr_fused(PrFusedArgs<CT> a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t V = a.out.V;
+  OpPr<CT> op{a.acc, a.contrib};
+  OutBuilder none{};
+  none.mode = OUT_NONE;
+  int64_t it = 0;
+  double l1 = INFINITY;
+  while (!(it >= a.max_iters || l1 < a.tol)) {
+    if (a.mode == 0 || a.mode == 1) {
+      EdgeArgs<OpPr<CT>> ea{a.coo, InView{-1}, op, none, 0};
+      if (a.mode == 0) {
+        edge_range(ea, 0, a.coo.E, tid, nth);
+      } else {
+        int64_t lo = 0;
+        for (int64_t s = 0; s < a.nseg; ++s) {
+          edge_range(ea, lo, a.seg_end[s], tid, nth);
+          lo = a.seg_end[s];
+          grid.sync();
+        }
+      }
+    } else if (a.mode == 2) {
+      for (int64_t v = tid; v < V; v += nth) {
+        double s = 0;
+        for (int64_t e = a.in.off[v]; e < a.in.off[v + 1]; ++e) s += (double)__ldg(a.contrib + __ldg(a.in.nbr + e));
+        a.acc[v] += s;
+      }
+    } else {
+      for (int64_t u = tid; u < V; u += nth) {
+        double c = (double)a.contrib[u];
+        for (int64_t e = a.out.off[u]; e < a.out.off[u + 1]; ++e) atomicAdd(a.acc + __ldg(a.out.nbr + e), c);
+      }
+    }
+    grid.sync();
+    pr_update_range(a.out.off, V, a.rank, a.contrib, a.acc, a.scal, it, a.damping, tid, nth);
+    grid.sync();
+    l1 = *((volatile double*)a.scal + 2 * it + 1);
+    ++it;
+  }
+  if (tid == 0) *a.iters_out = it;
+}
+
+template <class CT>
+static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
+                          int64_t max_iters, double tol, double damping, double* ranks_out,
+                          Runtime& rt) {
+  const int64_t V = g.V;
+  const int dev = g.dev;
+  cudaStream_t st = rt.stream;
+  g.ensure_out();  // out-degrees
+  const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
+  DevBuf<double> rank(V), acc(V), scal(2 * (iters_cap + 2));
+  DevBuf<CT> contrib(V);
+  scal.zero(st);
+  k_pr_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(g.out_off.p, V, rank.p, contrib.p, acc.p, scal.p);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  const gg_schedule& s = b.s1;
+  int64_t it = 0;
+  if (!fusion) {
+    double l1 = INFINITY;
+    gg_udf_state ust{acc.p, contrib.p, 0};
+    const int udf = sizeof(CT) == 8 ? UDF_PR : UDF_PR32;
+    while (!(it >= max_iters || l1 < tol)) {
+      rt.edge_begin();
+      edgeset_apply(&rt, udf, ust, false, nullptr, b, false, false);
+      rt.edge_end();
+      k_pr_update<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(g.out_off.p, V, rank.p, contrib.p, acc.p,
+                                                             scal.p, it, damping);
+      GG_LAUNCH_CHECK();
+      count_launch();
+      ++it;
+      rt.stats.rounds += 1;
+      if (tol > 0.0) {
+        GG_CUDA(cudaMemcpyAsync(&l1, scal.p + 2 * (it - 1) + 1, 8, cudaMemcpyDeviceToHost, st));
+        GG_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+  } else {
+    PrFusedArgs<CT> a{};
+    a.out = g.out_view();
+    if (s.load_balance != GG_LB_EDGE_ONLY && s.direction == GG_PULL) a.in = g.in_view();
+    a.coo = g.coo_view();
+    if (s.load_balance == GG_LB_EDGE_ONLY) {
+      a.mode = 0;
+      if (s.blocking) {
+        int64_t n = s.blocking_size > 0 ? s.blocking_size : default_blocking_size(g);
+        Blocked* bl = blocked_for(const_cast<Graph&>(g), n);
+        a.coo = CooView{bl->src.p, bl->dst.p, nullptr, bl->E};
+        a.seg_end = bl->seg_end.p;
+        a.nseg = bl->nseg;
+        a.mode = 1;
+      } else if (!g.has_coo) {
+        fail(GG_ERR_ENGINE, "graph COO view was dropped");
+      }
+    } else {
+      a.mode = s.direction == GG_PULL ? 2 : 3;
+    }
+    a.rank = rank.p;
+    a.contrib = contrib.p;
+    a.acc = acc.p;
+    a.scal = scal.p;
+    a.max_iters = max_iters;
+    a.tol = tol;
+    a.damping = damping;
+    DevBuf<int64_t> iters(1);
+    a.iters_out = iters.p;
+    int per_sm = 0;
+    GG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_pr_fused<CT>, 256, 0));
+    void* args[] = {&a};
+    rt.edge_begin();
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pr_fused<CT>, per_sm * sm_count(dev), 256, args,
+                                        0, st));
+    rt.edge_end();
+    count_launch();
+    GG_CUDA(cudaMemcpyAsync(&it, iters.p, 8, cudaMemcpyDeviceToHost, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+    rt.stats.dispatch_count += 1;
+    rt.stats.rounds += it;
+    rt.stats.edges_traversed += it * g.E;
+    for (int64_t k = 0; k < it; ++k) rt.stats.direction_log.push_back(s.direction);
+  }
+  GG_CUDA(cudaMemcpyAsync(ranks_out, rank.p, V * sizeof(double), cudaMemcpyDefault, st));
+  GG_CUDA(cudaStreamSynchronize(st));
+}
+
+void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
+                  int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
+                  bool fp32_contrib) {
+  if (g.V == 0) fail(GG_ERR_VALUE, "empty graph");
+  if (b.is_hybrid)
+    fail(GG_ERR_SCHEDULE, "label 's0:s1' of pagerank takes a SimpleGPUSchedule (hybrid direction "
+                          "switching applies to bfs/bc)");
+  check_binding(b);
+  DeviceGuard guard(g.dev);
+  if (fp32_contrib)
+    pagerank_impl<float>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt);
+  else
+    pagerank_impl<double>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt);
+}
+
+}  // namespace gg

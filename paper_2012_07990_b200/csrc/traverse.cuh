@@ -1,0 +1,786 @@
+// traverse.cuh — device side of edgeset.apply (reference engine.py:418-608).
+//
+// One template family per load-balancing strategy (engine.py:32-256), for
+// both directions, plus the flat / blocked COO paths (engine.py:558-608,
+// blocking.py:116-186).  A traversal is parameterised by an Op functor (the
+// named device UDF, see ops.cuh) and an OutBuilder (output frontier creation
+// with dedup, engine.py:279-397).
+//
+// Graph layout in HBM (built once, graph.cu):
+//   CSR-out  out_off int64[V+1], out_nbr int32[E], out_w uint32[E]
+//   CSR-in   in_off  int64[V+1], in_nbr  int32[E], in_w  uint32[E]
+//   COO      src int32[E], dst int32[E], w uint32[E]   (load order)
+// Frontiers: SPARSE int32 queue + u64 device count; BITMAP u32 words (same
+// byte/bit order as the reference's bytearray, frontier.py:184); BOOLMAP u8.
+#pragma once
+#include "common.cuh"
+#include <cooperative_groups.h>
+
+namespace gg {
+namespace cg = cooperative_groups;
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// Read-only views
+// ---------------------------------------------------------------------------
+struct CsrView {
+  const int64_t* off;
+  const int32_t* nbr;
+  const uint32_t* w;  // may be null
+  int64_t V;
+};
+
+struct CooView {
+  const int32_t* src;
+  const int32_t* dst;
+  const uint32_t* w;
+  int64_t E;
+};
+
+// Input frontier view. repr -1 = every vertex active (input None).
+struct InView {
+  int repr;
+  const int32_t* ids;
+  const unsigned long long* count;
+  const uint32_t* bits;
+  const uint8_t* bools;
+
+  __device__ __forceinline__ int64_t size() const { return (int64_t)*count; }
+  __device__ __forceinline__ bool member(int32_t u) const {
+    if (repr == GG_BITMAP) return (__ldg(bits + (u >> 5)) >> (u & 31)) & 1u;
+    if (repr == GG_BOOLMAP) return __ldg(bools + u) != 0;
+    return true;  // all active
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Output frontier builder (engine.py:279-397 + frontier.py:34-118).
+// ---------------------------------------------------------------------------
+enum { OUT_NONE = -1 };
+enum { DEDUP_NONE = 0, DEDUP_COUNTERS = 1, DEDUP_MARK_BITS = 2, DEDUP_MARK_BYTES = 3,
+       DEDUP_SLOT = 4 };
+
+__device__ __forceinline__ bool test_and_set_bit(uint32_t* words, int32_t v) {
+  uint32_t m = 1u << (v & 31);
+  return (atomicOr(words + (v >> 5), m) & m) != 0;
+}
+__device__ __forceinline__ bool test_and_set_byte(uint8_t* bytes, int32_t v) {
+  // byte test-and-set through the aligned 32-bit word holding it
+  uint32_t* w = reinterpret_cast<uint32_t*>(bytes + (v & ~3));
+  uint32_t m = 1u << ((v & 3) * 8);
+  return (atomicOr(w, m) & m) != 0;
+}
+
+struct OutBuilder {
+  int mode;   // OUT_NONE or GG_CREATE_*
+  int dedup;  // DEDUP_*
+  int32_t* queue;
+  unsigned long long* qcount;
+  uint32_t* bits;
+  uint8_t* bools;
+  int32_t* stamps;
+  int32_t round;
+  uint32_t* mark_bits;
+  uint8_t* mark_bytes;
+
+  __device__ __forceinline__ bool accept(int32_t v) const {
+    switch (dedup) {
+      case DEDUP_COUNTERS:
+        if (*((volatile int32_t*)stamps + v) == round) return false;
+        return atomicExch(stamps + v, round) != round;
+      case DEDUP_MARK_BITS: return !test_and_set_bit(mark_bits, v);
+      case DEDUP_MARK_BYTES: return !test_and_set_byte(mark_bytes, v);
+      default: return true;
+    }
+  }
+
+  // ctx.enqueue(v) (runtime.py:319-323): returns the dedup decision.
+  __device__ __forceinline__ bool emit(int32_t v) const {
+    if (mode == GG_CREATE_FUSED) {
+      bool ok = accept(v);
+      // warp-aggregated append: one atomic per converged group of lanes
+      cg::coalesced_group g = cg::coalesced_threads();
+      unsigned ballot = g.ballot(ok);
+      unsigned long long base = 0;
+      if (g.thread_rank() == 0 && ballot) base = atomicAdd(qcount, (unsigned long long)__popc(ballot));
+      base = g.shfl(base, 0);
+      if (ok) queue[base + __popc(ballot & ((1u << g.thread_rank()) - 1))] = v;
+      return ok;
+    }
+    if (mode == GG_CREATE_UNFUSED_BOOLMAP) {
+      if (dedup == DEDUP_SLOT) return !test_and_set_byte(bools, v);
+      if (dedup != DEDUP_NONE && !accept(v)) return false;
+      bools[v] = 1;
+      return true;
+    }
+    if (mode == GG_CREATE_UNFUSED_BITMAP) {
+      if (dedup == DEDUP_SLOT) return !test_and_set_bit(bits, v);
+      if (dedup != DEDUP_NONE && !accept(v)) return false;
+      atomicOr(bits + (v >> 5), 1u << (v & 31));
+      return true;
+    }
+    return false;
+  }
+};
+
+// Edges scanned (RunStats.edges_traversed): one atomic per warp.
+__device__ __forceinline__ void add_scanned(unsigned long long* ctr, int64_t n) {
+  unsigned long long s = (unsigned long long)n;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane_id() == 0 && s) atomicAdd(ctr, s);
+}
+
+// Active id at position i of the input (input None => identity).
+__device__ __forceinline__ int32_t active_at(const InView& in, int64_t i) {
+  return in.repr == -1 ? (int32_t)i : __ldg(in.ids + i);
+}
+__device__ __forceinline__ int64_t active_count(const InView& in, int64_t V) {
+  return in.repr == -1 ? V : in.size();
+}
+
+// Largest j in [0, n) with key(j) <= x over a sorted array (binary search).
+template <class F>
+__device__ __forceinline__ int upper_idx(F key, int n, int64_t x) {
+  int lo = 0, hi = n;  // invariant: answer in [lo, hi)
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (key(mid) <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// ===========================================================================
+// PUSH (engine.py:463-503): per active source, scan out-edges, filter dst,
+// udf with atomic helpers.
+// ===========================================================================
+template <class Op>
+struct PushArgs {
+  CsrView g;
+  InView in;
+  Op op;
+  OutBuilder out;
+  int use_filter;
+  unsigned long long* scanned;
+};
+
+template <class Op>
+__device__ __forceinline__ void push_edge(const PushArgs<Op>& a, int32_t u, int64_t e) {
+  int32_t v = __ldg(a.g.nbr + e);
+  if (a.use_filter && !a.op.filter(v)) return;
+  uint32_t w = a.g.w ? __ldg(a.g.w + e) : 0u;
+  a.op.push(u, v, w, a.out);
+}
+
+// VERTEX_BASED (engine.py:179-183): one thread per active vertex.
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_vb(PushArgs<Op> a) {
+  const int64_t n = active_count(a.in, a.g.V);
+  int64_t sc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t u = active_at(a.in, i);
+    int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
+    sc += hi - lo;
+    for (int64_t e = lo; e < hi; ++e) push_edge(a, u, e);
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// WM (engine.py:167-176): each warp takes 32 contiguous active vertices and
+// processes their concatenated edge lists lane-cyclically (warp prefix sum +
+// shuffle binary search to find each edge's owner).
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_wm(PushArgs<Op> a) {
+  const int64_t n = active_count(a.in, a.g.V);
+  const int lane = lane_id();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t sc = 0;
+  for (int64_t base = warp * kWarp; base < n; base += nwarps * kWarp) {
+    int64_t i = base + lane;
+    int32_t u = -1;
+    int64_t lo = 0, deg = 0;
+    if (i < n) {
+      u = active_at(a.in, i);
+      lo = __ldg(a.g.off + u);
+      deg = __ldg(a.g.off + u + 1) - lo;
+    }
+    // inclusive warp scan of degrees
+    int64_t incl = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int64_t excl = incl - deg;
+    int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+    sc += deg;
+    for (int64_t k0 = 0; k0 < total; k0 += kWarp) {
+      const int64_t k = k0 + lane;
+      // owner = largest lane j with excl_j <= k (never a zero-degree lane
+      // when k < total); all lanes take part in every shuffle.
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        int64_t em = __shfl_sync(0xffffffffu, excl, j + step);
+        if (em <= k) j += step;
+      }
+      int32_t uj = __shfl_sync(0xffffffffu, u, j);
+      int64_t loj = __shfl_sync(0xffffffffu, lo, j);
+      int64_t exj = __shfl_sync(0xffffffffu, excl, j);
+      if (k < total) push_edge(a, uj, loj + (k - exj));
+    }
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// CM (engine.py:160-164): each CTA takes blockDim contiguous active vertices
+// and processes their concatenated edges cooperatively (CTA prefix sum in
+// shared memory + binary search).
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_cm(PushArgs<Op> a) {
+  __shared__ int64_t s_excl[257];
+  __shared__ int64_t s_lo[256];
+  __shared__ int32_t s_u[256];
+  const int64_t n = active_count(a.in, a.g.V);
+  int64_t sc = 0;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    int64_t deg = 0;
+    if (i < n) {
+      int32_t u = active_at(a.in, i);
+      s_u[threadIdx.x] = u;
+      s_lo[threadIdx.x] = __ldg(a.g.off + u);
+      deg = __ldg(a.g.off + u + 1) - s_lo[threadIdx.x];
+    } else {
+      s_u[threadIdx.x] = -1;
+      s_lo[threadIdx.x] = 0;
+    }
+    sc += deg;
+    s_excl[threadIdx.x + 1] = deg;
+    if (threadIdx.x == 0) s_excl[0] = 0;
+    __syncthreads();
+    // simple Hillis-Steele scan over 256 entries (shared memory)
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+      int64_t t = (threadIdx.x + 1 > (unsigned)o) ? s_excl[threadIdx.x + 1 - o] : 0;
+      __syncthreads();
+      s_excl[threadIdx.x + 1] += t;
+      __syncthreads();
+    }
+    const int64_t total = s_excl[blockDim.x];
+    const int cnt = (int)blockDim.x;
+    for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
+      int j = upper_idx([&](int m) { return s_excl[m]; }, cnt, k);
+      // skip zero-degree owners that share the same prefix
+      while (j + 1 < cnt && s_excl[j + 1] <= k) ++j;
+      push_edge(a, s_u[j], s_lo[j] + (k - s_excl[j]));
+    }
+    __syncthreads();
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// STRICT (engine.py:97-122): exact edge balance.  `prefix` is the exclusive
+// degree prefix over the active list (length n+1, computed by a device scan);
+// each thread takes a contiguous run of `per` edges and locates its first
+// owner by binary search.
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_strict(PushArgs<Op> a, const int64_t* prefix,
+                                                      int64_t per) {
+  const int64_t n = active_count(a.in, a.g.V);
+  const int64_t total = prefix[n];
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t elo = t * per; elo < total; elo += (int64_t)gridDim.x * blockDim.x * per) {
+    int64_t ehi = min(total, elo + per);
+    // largest i with prefix[i] <= elo
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (__ldg(prefix + mid) <= elo) lo = mid; else hi = mid;
+    }
+    for (int64_t i = lo; i < n; ++i) {
+      int64_t p0 = __ldg(prefix + i), p1 = __ldg(prefix + i + 1);
+      if (p0 >= ehi) break;
+      int64_t a0 = max(elo, p0), a1 = min(ehi, p1);
+      if (a0 >= a1) continue;
+      int32_t u = active_at(a.in, i);
+      int64_t off = __ldg(a.g.off + u);
+      for (int64_t k = a0; k < a1; ++k) push_edge(a, u, off + (k - p0));
+    }
+  }
+  if (t == 0) atomicAdd(a.scanned, (unsigned long long)total);
+}
+
+// TWC (engine.py:125-157): global buckets by degree (> cta: CTA queue,
+// > warp: warp queue, else thread queue; strictly greater promotion).
+struct TwcQueues {
+  int32_t* q[3];               // 0 thread, 1 warp, 2 cta
+  unsigned long long* cnt;     // [3]
+};
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_bin(PushArgs<Op> a, TwcQueues q, int cta) {
+  const int64_t n = active_count(a.in, a.g.V);
+  int64_t sc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t u = active_at(a.in, i);
+    int64_t deg = __ldg(a.g.off + u + 1) - __ldg(a.g.off + u);
+    sc += deg;
+    int b = deg > cta ? 2 : (deg > kWarp ? 1 : 0);
+    cg::coalesced_group g = cg::coalesced_threads();
+    cg::coalesced_group gb = cg::labeled_partition(g, b);
+    unsigned long long base = 0;
+    if (gb.thread_rank() == 0) base = atomicAdd(q.cnt + b, (unsigned long long)gb.size());
+    base = gb.shfl(base, 0);
+    q.q[b][base + gb.thread_rank()] = u;
+  }
+  add_scanned(a.scanned, sc);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_thread(PushArgs<Op> a, const int32_t* qu,
+                                                    const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t u = qu[i];
+    int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
+    for (int64_t e = lo; e < hi; ++e) push_edge(a, u, e);
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t* qu,
+                                                  const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    int32_t u = qu[i];
+    int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
+    for (int64_t e = lo + lane_id(); e < hi; e += kWarp) push_edge(a, u, e);
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
+                                                 const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    int32_t u = qu[i];
+    int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) push_edge(a, u, e);
+  }
+}
+
+// ETWC (engine.py:51-85, 186-193; paper Alg. 3).  Each CTA takes blockDim
+// contiguous active vertices; every vertex's range is split into a
+// CTA-multiple (Q2), warp-multiple (Q1) and remainder (Q0) chunk, queued in
+// shared memory (warp ballot + CTA prefix for slots), then the stages run in
+// order 0, 1, 2 with thread / warp / CTA cooperative processing.
+struct EtwcEntry {
+  int64_t lo, hi;
+  int32_t u;
+};
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_etwc(PushArgs<Op> a, int cta) {
+  __shared__ EtwcEntry s_q[3][256];
+  __shared__ int s_n[3];
+  const int64_t n = active_count(a.in, a.g.V);
+  const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t sc = 0;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x < 3) s_n[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t i = base + threadIdx.x;
+    int64_t start = 0, end = 0;
+    int32_t u = -1;
+    if (i < n) {
+      u = active_at(a.in, i);
+      start = __ldg(a.g.off + u);
+      end = __ldg(a.g.off + u + 1);
+    }
+    int64_t size = end - start;
+    sc += size;
+    int64_t e2 = (size / cta) * cta;
+    int64_t e1 = ((size - e2) / kWarp) * kWarp;
+    int64_t e0 = size - e2 - e1;
+    EtwcEntry c2{start, start + e2, u}, c1{start + e2, start + e2 + e1, u},
+        c0{start + e2 + e1, end, u};
+    bool has[3] = {e0 > 0, e1 > 0, e2 > 0};
+    const EtwcEntry* ent[3] = {&c0, &c1, &c2};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      unsigned b = __ballot_sync(0xffffffffu, has[q]);
+      int slot = 0;
+      if (lane == 0 && b) slot = atomicAdd(&s_n[q], __popc(b));
+      slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(b & ((1u << lane) - 1));
+      if (has[q]) s_q[q][slot] = *ent[q];
+    }
+    __syncthreads();
+    // stage 0: individual threads
+    for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
+      EtwcEntry c = s_q[0][k];
+      for (int64_t e = c.lo; e < c.hi; ++e) push_edge(a, c.u, e);
+    }
+    // stage 1: warps
+    for (int k = wid; k < s_n[1]; k += nw) {
+      EtwcEntry c = s_q[1][k];
+      for (int64_t e = c.lo + lane; e < c.hi; e += kWarp) push_edge(a, c.u, e);
+    }
+    // stage 2: whole CTA
+    for (int k = 0; k < s_n[2]; ++k) {
+      EtwcEntry c = s_q[2][k];
+      for (int64_t e = c.lo + threadIdx.x; e < c.hi; e += blockDim.x) push_edge(a, c.u, e);
+    }
+    __syncthreads();
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// ===========================================================================
+// PULL (engine.py:506-555): per destination passing the filter, scan in-edges,
+// test source membership, udf with owner-write rights.  The op reduces over a
+// destination's in-edges into an accumulator (register/shuffle/shared), and
+// finishes with one owner write.
+// ===========================================================================
+template <class Op>
+struct PullArgs {
+  CsrView g;  // CSR-in
+  InView in;  // membership (dense) or all
+  Op op;
+  OutBuilder out;
+  int use_filter;
+  unsigned long long* scanned;
+};
+
+template <class Op>
+__device__ __forceinline__ bool pull_visit(const PullArgs<Op>& a, typename Op::Acc& acc,
+                                           int64_t e) {
+  int32_t u = __ldg(a.g.nbr + e);
+  if (!a.in.member(u)) return false;
+  uint32_t w = a.g.w ? __ldg(a.g.w + e) : 0u;
+  return a.op.visit(acc, u, w);
+}
+
+// VERTEX_BASED: thread per destination (early exit when the op says so).
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_vb(PullArgs<Op> a) {
+  int64_t sc = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.g.V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (a.use_filter && !a.op.filter((int32_t)v)) continue;
+    int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
+    sc += hi - lo;
+    typename Op::Acc acc = a.op.init();
+    for (int64_t e = lo; e < hi; ++e)
+      if (pull_visit(a, acc, e)) break;
+    a.op.finish((int32_t)v, acc, a.out);
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// Warp-cooperative reduction of one destination's in-range [lo, hi).
+template <class Op>
+__device__ __forceinline__ typename Op::Acc pull_warp_range(const PullArgs<Op>& a, int64_t lo,
+                                                            int64_t hi) {
+  typename Op::Acc acc = a.op.init();
+  for (int64_t e0 = lo; e0 < hi; e0 += kWarp) {
+    bool stop = false;
+    if (e0 + lane_id() < hi) stop = pull_visit(a, acc, e0 + lane_id());
+    if (Op::kEarlyExit && __any_sync(0xffffffffu, stop)) break;
+  }
+  return Op::warp_reduce(acc);
+}
+
+// WM: warps take contiguous destination chunks; each destination's in-list
+// is reduced by the whole warp.
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_wm(PullArgs<Op> a) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t chunk = (a.g.V + nwarps - 1) / nwarps;
+  int64_t sc = 0;
+  for (int64_t v = warp * chunk; v < min(a.g.V, (warp + 1) * chunk); ++v) {
+    if (a.use_filter && !a.op.filter((int32_t)v)) continue;
+    int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
+    if (lane_id() == 0) sc += hi - lo;
+    typename Op::Acc acc = pull_warp_range(a, lo, hi);
+    if (lane_id() == 0) a.op.finish((int32_t)v, acc, a.out);
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// Block-wide reduction helper (accumulators are tiny PODs).
+template <class Op>
+__device__ __forceinline__ typename Op::Acc block_reduce(typename Op::Acc acc) {
+  __shared__ typename Op::Acc s_part[32];
+  acc = Op::warp_reduce(acc);
+  const int wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane_id() == 0) s_part[wid] = acc;
+  __syncthreads();
+  typename Op::Acc r = s_part[0];
+  for (int k = 1; k < (int)(blockDim.x >> 5); ++k) r = Op::combine(r, s_part[k]);
+  return r;
+}
+
+// CM: CTAs take contiguous destination chunks; each destination's in-list is
+// reduced by the whole CTA.
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_cm(PullArgs<Op> a) {
+  __shared__ int s_keep;
+  const int64_t chunk = (a.g.V + gridDim.x - 1) / gridDim.x;
+  int64_t sc = 0;
+  for (int64_t v = blockIdx.x * chunk; v < min(a.g.V, (blockIdx.x + 1) * chunk); ++v) {
+    if (threadIdx.x == 0) s_keep = !a.use_filter || a.op.filter((int32_t)v);
+    __syncthreads();
+    bool keep = s_keep;
+    __syncthreads();
+    if (!keep) continue;
+    int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
+    if (threadIdx.x == 0) sc += hi - lo;
+    typename Op::Acc acc = a.op.init();
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, e);
+    acc = block_reduce<Op>(acc);
+    if (threadIdx.x == 0) a.op.finish((int32_t)v, acc, a.out);
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// STRICT (engine.py:216-225): edge-balanced destination spans snapped to
+// vertex boundaries (each destination keeps one owner).  `span_start[t]` is
+// the first destination of span t (length nspans+1), computed on the device.
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_strict(PullArgs<Op> a, const int64_t* span_start,
+                                                     int64_t nspans) {
+  int64_t sc = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nspans;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t v = span_start[t]; v < span_start[t + 1]; ++v) {
+      if (a.use_filter && !a.op.filter((int32_t)v)) continue;
+      int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
+      sc += hi - lo;
+      typename Op::Acc acc = a.op.init();
+      for (int64_t e = lo; e < hi; ++e)
+        if (pull_visit(a, acc, e)) break;
+      a.op.finish((int32_t)v, acc, a.out);
+    }
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// TWC pull (engine.py:249-251): destinations binned by in-degree; the three
+// consumers reuse thread / warp / CTA reduction.
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_bin(PullArgs<Op> a, TwcQueues q, int cta) {
+  int64_t sc = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.g.V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (a.use_filter && !a.op.filter((int32_t)v)) continue;
+    int64_t deg = __ldg(a.g.off + v + 1) - __ldg(a.g.off + v);
+    sc += deg;
+    int b = deg > cta ? 2 : (deg > kWarp ? 1 : 0);
+    cg::coalesced_group g = cg::coalesced_threads();
+    cg::coalesced_group gb = cg::labeled_partition(g, b);
+    unsigned long long base = 0;
+    if (gb.thread_rank() == 0) base = atomicAdd(q.cnt + b, (unsigned long long)gb.size());
+    base = gb.shfl(base, 0);
+    q.q[b][base + gb.thread_rank()] = (int32_t)v;
+  }
+  add_scanned(a.scanned, sc);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_thread(PullArgs<Op> a, const int32_t* qv,
+                                                         const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = qv[i];
+    int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
+    typename Op::Acc acc = a.op.init();
+    for (int64_t e = lo; e < hi; ++e)
+      if (pull_visit(a, acc, e)) break;
+    a.op.finish(v, acc, a.out);
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_warp(PullArgs<Op> a, const int32_t* qv,
+                                                       const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    int32_t v = qv[i];
+    typename Op::Acc acc = pull_warp_range(a, __ldg(a.g.off + v), __ldg(a.g.off + v + 1));
+    if (lane_id() == 0) a.op.finish(v, acc, a.out);
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_cta(PullArgs<Op> a, const int32_t* qv,
+                                                      const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    int32_t v = qv[i];
+    int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
+    typename Op::Acc acc = a.op.init();
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, e);
+    acc = block_reduce<Op>(acc);
+    if (threadIdx.x == 0) a.op.finish(v, acc, a.out);
+  }
+}
+
+// ETWC pull (engine.py:252-255): chunked in-ranges stay inside one CTA.  Each
+// destination contributes at most one entry per stage; stage partials are
+// kept per destination slot in shared memory and combined by the owner
+// thread, which then performs the single owner write.
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_etwc(PullArgs<Op> a, int cta) {
+  __shared__ EtwcEntry s_q[3][256];
+  __shared__ int s_slot[3][256];  // queue entry -> destination slot
+  __shared__ typename Op::Acc s_part[3][256];
+  __shared__ int s_n[3];
+  const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t sc = 0;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < a.g.V;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x < 3) s_n[threadIdx.x] = 0;
+    const typename Op::Acc zero = a.op.init();
+    for (int q = 0; q < 3; ++q) s_part[q][threadIdx.x] = zero;
+    __syncthreads();
+    int64_t v = base + threadIdx.x;
+    bool keep = v < a.g.V && (!a.use_filter || a.op.filter((int32_t)v));
+    int64_t start = 0, end = 0;
+    if (keep) {
+      start = __ldg(a.g.off + v);
+      end = __ldg(a.g.off + v + 1);
+    }
+    int64_t size = end - start;
+    sc += size;
+    int64_t e2 = (size / cta) * cta;
+    int64_t e1 = ((size - e2) / kWarp) * kWarp;
+    int64_t e0 = size - e2 - e1;
+    EtwcEntry c[3] = {{start + e2 + e1, end, (int32_t)v}, {start + e2, start + e2 + e1, (int32_t)v},
+                      {start, start + e2, (int32_t)v}};
+    bool has[3] = {e0 > 0, e1 > 0, e2 > 0};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      unsigned b = __ballot_sync(0xffffffffu, has[q]);
+      int slot = 0;
+      if (lane == 0 && b) slot = atomicAdd(&s_n[q], __popc(b));
+      slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(b & ((1u << lane) - 1));
+      if (has[q]) {
+        s_q[q][slot] = c[q];
+        s_slot[q][slot] = threadIdx.x;
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
+      EtwcEntry ce = s_q[0][k];
+      typename Op::Acc acc = a.op.init();
+      for (int64_t e = ce.lo; e < ce.hi; ++e)
+        if (pull_visit(a, acc, e)) break;
+      s_part[0][s_slot[0][k]] = acc;
+    }
+    for (int k = wid; k < s_n[1]; k += nw) {
+      EtwcEntry ce = s_q[1][k];
+      typename Op::Acc acc = pull_warp_range(a, ce.lo, ce.hi);
+      if (lane == 0) s_part[1][s_slot[1][k]] = acc;
+    }
+    for (int k = 0; k < s_n[2]; ++k) {
+      EtwcEntry ce = s_q[2][k];
+      typename Op::Acc acc = a.op.init();
+      for (int64_t e = ce.lo + threadIdx.x; e < ce.hi; e += blockDim.x) pull_visit(a, acc, e);
+      acc = block_reduce<Op>(acc);
+      if (threadIdx.x == 0) s_part[2][s_slot[2][k]] = acc;
+    }
+    __syncthreads();
+    if (keep) {
+      typename Op::Acc acc =
+          Op::combine(Op::combine(s_part[0][threadIdx.x], s_part[1][threadIdx.x]), s_part[2][threadIdx.x]);
+      a.op.finish((int32_t)v, acc, a.out);
+    }
+    __syncthreads();
+  }
+  add_scanned(a.scanned, sc);
+}
+
+// ===========================================================================
+// EDGE_ONLY (engine.py:558-608): flat COO, source membership + dst filter per
+// arc, always the atomic interface.  Vectorised 16-byte loads of src/dst.
+// ===========================================================================
+template <class Op>
+struct EdgeArgs {
+  CooView coo;
+  InView in;  // dense membership or all
+  Op op;
+  OutBuilder out;
+  int use_filter;
+};
+
+template <class Op>
+__device__ __forceinline__ void edge_one(const EdgeArgs<Op>& a, int32_t u, int32_t v, int64_t e) {
+  if (!a.in.member(u)) return;
+  if (a.use_filter && !a.op.filter(v)) return;
+  uint32_t w = a.coo.w ? __ldg(a.coo.w + e) : 0u;
+  a.op.push(u, v, w, a.out);
+}
+
+template <class Op>
+__device__ __forceinline__ void edge_range(const EdgeArgs<Op>& a, int64_t lo, int64_t hi,
+                                           int64_t tid, int64_t nthreads) {
+  // scalar head until 16-byte alignment of both arrays, vector body, tail
+  int64_t head = lo;
+  while (head < hi && (((uintptr_t)(a.coo.src + head)) & 15)) ++head;
+  if (((uintptr_t)(a.coo.dst + head) & 15) != 0) head = hi;  // misaligned pair: scalar
+  for (int64_t e = lo + tid; e < head; e += nthreads)
+    edge_one(a, __ldg(a.coo.src + e), __ldg(a.coo.dst + e), e);
+  int64_t nvec = (hi - head) >> 2;
+  const int4* s4 = reinterpret_cast<const int4*>(a.coo.src + head);
+  const int4* d4 = reinterpret_cast<const int4*>(a.coo.dst + head);
+  for (int64_t k = tid; k < nvec; k += nthreads) {
+    int4 s = ld_stream4(s4 + k), d = ld_stream4(d4 + k);
+    int64_t e = head + 4 * k;
+    edge_one(a, s.x, d.x, e);
+    edge_one(a, s.y, d.y, e + 1);
+    edge_one(a, s.z, d.z, e + 2);
+    edge_one(a, s.w, d.w, e + 3);
+  }
+  for (int64_t e = head + 4 * nvec + tid; e < hi; e += nthreads)
+    edge_one(a, __ldg(a.coo.src + e), __ldg(a.coo.dst + e), e);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) k_edge_only(EdgeArgs<Op> a) {
+  edge_range(a, 0, a.coo.E, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+             (int64_t)gridDim.x * blockDim.x);
+}
+
+// EdgeBlocking Alg. 2 (blocking.py:116-186): segments in order, the whole
+// grid cooperates on one segment, grid barrier between segments.  Launched
+// cooperatively (one dispatch).
+template <class Op>
+__global__ void __launch_bounds__(256) k_edge_blocked(EdgeArgs<Op> a, const int64_t* seg_end,
+                                                      int64_t nseg) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  int64_t lo = 0;
+  for (int64_t s = 0; s < nseg; ++s) {
+    int64_t hi = seg_end[s];
+    edge_range(a, lo, hi, tid, nthreads);
+    lo = hi;
+    grid.sync();
+  }
+}
+
+}  // namespace gg

@@ -1,0 +1,71 @@
+"""Device graph construction vs the reference layout (graphio.from_coo)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import gen
+from tests.util import arrays
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gg():
+    import paper_2012_07990_b200 as gg
+    return gg
+
+
+def test_csr_views_equal_stable_counting_sort(gg, golden_small):
+    for name, rec in golden_small["graphs"].items():
+        V, s, d, w = arrays(rec)
+        g = gg.Graph.from_coo(V, s, d, w)
+        off, nbr, ww = oracle.csr(V, s, d, w)
+        assert g.out_offsets.tolist() == off.tolist(), name
+        assert g.out_neighbors.tolist() == nbr.tolist(), name
+        ioff, inbr, iww = oracle.csr(V, d, s, w)
+        assert g.in_offsets.tolist() == ioff.tolist(), name
+        assert g.in_neighbors.tolist() == inbr.tolist(), name
+        if w is not None:
+            assert g.out_weights.tolist() == ww.tolist()
+            assert g.in_weights.tolist() == iww.tolist()
+
+
+def test_out_of_range_ids_rejected(gg):
+    with pytest.raises(ValueError, match="out of range"):
+        gg.Graph.from_coo(3, [0, 5], [1, 2])
+
+
+def test_device_generators_match_host_replicas(gg):
+    g = gg.generate_rmat(12, 16, seed=2)
+    V, s, d = gen.rmat(12, 16, seed=2)
+    assert np.array_equal(g.coo_src, s) and np.array_equal(g.coo_dst, d)
+    gw = gg.generate_rmat(10, 4, seed=9, weights=True)
+    assert np.array_equal(gw.coo_weights, gen.weights(gw.num_edges, 9))
+    gs = gg.generate_rmat(12, 16, seed=2, symmetrize=True)
+    from paper_2012_07990_b200.graphio import symmetrize_coo
+    ss, dd, _, _ = symmetrize_coo(s, d)
+    assert np.array_equal(gs.coo_src, ss) and np.array_equal(gs.coo_dst, dd)
+    gr = gg.generate_grid(33)
+    Vg, sg, dg = gen.grid(33)
+    assert gr.num_vertices == Vg and np.array_equal(gr.coo_src, sg)
+    assert np.array_equal(gr.coo_dst, dg)
+    assert gr.num_edges == 4 * 33 * 32
+
+
+def test_sort_by_source_keeps_stable_order(gg):
+    g = gg.generate_rmat(10, 8, seed=3, sort_by_source=True)
+    V, s, d = gen.rmat(10, 8, seed=3)
+    s2, d2, _ = gen.sort_by_source(s, d)
+    assert np.array_equal(g.coo_src, s2) and np.array_equal(g.coo_dst, d2)
+
+
+def test_block_edges_matches_reference(gg, golden_small):
+    for case in golden_small["cases"]:
+        if case["algo"] != "block_edges":
+            continue
+        V, s, d, w = arrays(golden_small["graphs"][case["graph"]])
+        g = gg.Graph.from_coo(V, s, d, w)
+        bg = gg.block_edges(g, case["n"])
+        assert bg.segment_start == case["segment_start"]
+        assert bg.edges_src == case["src"] and bg.edges_dst == case["dst"]

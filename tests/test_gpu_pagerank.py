@@ -1,0 +1,120 @@
+"""PageRank on the device vs the reference (golden) and the oracle.
+
+Tolerance (north star): <= 1e-6 max relative error per vertex.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import gen
+from tests.conftest import GOLDEN
+from tests.util import arrays, max_rel_err, program_with, sched_from
+
+pytestmark = pytest.mark.gpu
+PR_TOL = 1e-6
+
+LBS = ["VERTEX_BASED", "CM", "WM", "STRICT", "EDGE_ONLY", "ETWC", "TWC"]
+
+
+@pytest.fixture(scope="module")
+def gg():
+    import paper_2012_07990_b200 as gg
+    return gg
+
+
+def _graph(gg, rec):
+    V, s, d, w = arrays(rec)
+    return gg.Graph.from_coo(V, s, d, w, symmetric=rec["symmetric"])
+
+
+def test_pagerank_golden_cases(gg, golden_small):
+    n = 0
+    for case in golden_small["cases"]:
+        if case["algo"] != "pagerank":
+            continue
+        g = _graph(gg, golden_small["graphs"][case["graph"]])
+        s = sched_from(case["schedule"])
+        r = gg.pagerank(g, program_with(s), max_iters=case["max_iters"],
+                        tolerance=case["tolerance"])
+        assert max_rel_err(r.values, case["ranks"]) < PR_TOL, (case["graph"], case["schedule"])
+        st = case["stats"]
+        assert r.stats.rounds == st["rounds"]
+        assert r.stats.dispatch_count == st["dispatch_count"]
+        assert r.stats.edges_traversed == st["edges_traversed"]
+        assert r.stats.direction_log == st["direction_log"]
+        n += 1
+    assert n >= 20
+
+
+@pytest.mark.parametrize("lb", LBS)
+@pytest.mark.parametrize("direction", ["PUSH", "PULL"])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_pagerank_every_schedule_matches_oracle(gg, lb, direction, fusion):
+    V, s, d = gen.rmat(10, 8, seed=11)
+    g = gg.Graph.from_coo(V, s, d)
+    want, _ = oracle.pagerank(V, s, d, 25, 0.0)
+    sch = gg.Schedule(direction=direction, load_balance=lb)
+    r = gg.pagerank(g, program_with(sch, fusion), max_iters=25, tolerance=0.0)
+    assert max_rel_err(r.values, want) < PR_TOL
+    assert r.stats.rounds == 25
+    assert r.stats.dispatch_count == (1 if fusion else 25)
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 1000, None])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_pagerank_edge_blocking_matches_oracle(gg, n, fusion):
+    V, s, d = gen.rmat(11, 8, seed=12)
+    g = gg.Graph.from_coo(V, s, d)
+    want, _ = oracle.pagerank(V, s, d, 20, 0.0)
+    sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True, blocking_size=n)
+    r = gg.pagerank(g, program_with(sch, fusion), max_iters=20, tolerance=0.0)
+    assert max_rel_err(r.values, want) < PR_TOL
+
+
+def test_c1_rmat16_device_generator_and_ranks(gg):
+    """C1 (BASELINE configs[0]): the device RMAT generator is bit-identical to
+    the fixture's edge list and 20 iterations match the reference's ranks."""
+    z = np.load(os.path.join(GOLDEN, "c1_pagerank_rmat16.npz"))
+    g = gg.generate_rmat(16, 16, seed=1)
+    s, d = g.coo_src, g.coo_dst
+    assert hashlib.sha256(s.tobytes() + d.tobytes()).hexdigest() == str(z["edge_sha256"])
+    for sch in (None, gg.Schedule(direction="PULL", load_balance="STRICT"),
+                gg.Schedule(load_balance="EDGE_ONLY", blocking=True)):
+        r = gg.pagerank(g, program_with(sch), max_iters=20, tolerance=0.0)
+        assert max_rel_err(r.values, z["ranks"]) < PR_TOL
+    r32 = gg.pagerank(g, None, max_iters=20, tolerance=0.0, contrib_fp32=True)
+    assert max_rel_err(r32.values, z["ranks"]) < PR_TOL
+
+
+def test_pagerank_tolerance_stops_early(gg, golden_small):
+    rec = golden_small["graphs"]["rs70"]
+    g = _graph(gg, rec)
+    V, s, d, _ = arrays(rec)
+    want, it = oracle.pagerank(V, s, d, 100, 1e-9)
+    r = gg.pagerank(g)  # reference defaults: max_iters=100, tolerance=1e-9
+    assert r.stats.rounds == it
+    assert max_rel_err(r.values, want) < PR_TOL
+
+
+def test_pagerank_mass_conserved_each_iteration(gg):
+    from paper_2012_07990_b200.graphio import Graph
+    rng = np.random.default_rng(3)
+    s = rng.integers(0, 40, 120)
+    d = rng.integers(0, 40, 120)
+    g = Graph.from_coo(40, s, d)
+    sums = []
+    gg.pagerank(g, max_iters=25, tolerance=0.0, on_iteration=lambda r: sums.append(sum(r)))
+    assert len(sums) == 25
+    assert all(abs(x - 1.0) <= 1e-12 for x in sums)
+
+
+def test_pagerank_errors(gg):
+    g = gg.Graph.from_coo(2, [0], [1])
+    with pytest.raises(gg.ScheduleError, match="hybrid"):
+        gg.pagerank(g, gg.ScheduleProgram({"s0:s1": gg.HybridSchedule()}))
+    with pytest.raises(gg.ScheduleError, match="not exposed"):
+        gg.pagerank(g, gg.ScheduleProgram({"nope": gg.Schedule()}))
