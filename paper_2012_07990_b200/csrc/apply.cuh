@@ -1,0 +1,204 @@
+// apply.cuh — the edgeset.apply dispatcher templates (engine.py:418-608),
+// shared by every driver translation unit (BFS, PR, SSSP, CC, BC).
+#pragma once
+#include "engine.cuh"
+
+namespace gg {
+
+int max_coop_blocks(const void* fn, int block, int dev, size_t smem = 0);
+void strict_prefix(Runtime* rt, const InView& in, int64_t n);
+void strict_spans(Runtime* rt, int64_t nspans);
+void clear_marks(Runtime* rt, Frontier* out, const OutBuilder& ob);
+Frontier* converted_view(Runtime* rt, Frontier* in, int repr);
+void twc_queues(Runtime* rt, TwcQueues* q);
+OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out);
+void dense_size_on_device(Frontier* f, cudaStream_t s);
+
+template <class Op>
+void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
+                     int64_t n_host, const OutBuilder& out) {
+  const Graph* g = rt->g;
+  cudaStream_t st = rt->stream;
+  PushArgs<Op> a{g->out_view(), in, op, out, use_filter ? 1 : 0, rt->scanned.p};
+  const int dev = rt->dev;
+  const int64_t work = n_host >= 0 ? n_host : g->V;
+  const int cta = rt->cfg.cta_size;
+  switch (s.load_balance) {
+    case GG_LB_VERTEX_BASED:
+      k_push_vb<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_WM:
+      k_push_wm<Op><<<grid_for(work * 8, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_CM:
+      k_push_cm<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_ETWC:
+      k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
+      break;
+    case GG_LB_STRICT: {
+      const int64_t n = n_host >= 0 ? n_host : g->V;
+      strict_prefix(rt, in, n);
+      k_push_strict<Op><<<grid_for(g->E / 32 + 1, 256, dev), 256, 0, st>>>(a, rt->prefix.p, 32);
+      break;
+    }
+    case GG_LB_TWC: {
+      TwcQueues q;
+      twc_queues(rt, &q);
+      k_twc_bin<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q, cta);
+      a.scanned = rt->scanned.p;
+      k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
+      k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
+      k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      count_launch(3);
+      break;
+    }
+    default:
+      fail(GG_ERR_ENGINE, "no chunker for this load balance");
+  }
+  GG_LAUNCH_CHECK();
+  count_launch();
+}
+
+template <class Op>
+void run_pull(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
+                     const OutBuilder& out) {
+  const Graph* g = rt->g;
+  cudaStream_t st = rt->stream;
+  PullArgs<Op> a{g->in_view(), in, op, out, use_filter ? 1 : 0, rt->scanned.p};
+  const int dev = rt->dev;
+  const int64_t V = g->V;
+  const int cta = rt->cfg.cta_size;
+  switch (s.load_balance) {
+    case GG_LB_VERTEX_BASED:
+      k_pull_vb<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_WM:
+      k_pull_wm<Op><<<grid_for(V * 32, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_CM:
+      k_pull_cm<Op><<<grid_for(V * 256, 256, dev), 256, 0, st>>>(a);
+      break;
+    case GG_LB_ETWC:
+      k_pull_etwc<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, cta);
+      break;
+    case GG_LB_STRICT: {
+      const int64_t nspans = std::min<int64_t>(V > 0 ? V : 1, (int64_t)sm_count(dev) * 2048);
+      strict_spans(rt, nspans);
+      k_pull_strict<Op><<<grid_for(nspans, 256, dev), 256, 0, st>>>(a, rt->spans.p, nspans);
+      break;
+    }
+    case GG_LB_TWC: {
+      TwcQueues q;
+      twc_queues(rt, &q);
+      k_pull_twc_bin<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, q, cta);
+      k_pull_twc_thread<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
+      k_pull_twc_warp<Op><<<grid_for(V * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
+      k_pull_twc_cta<Op><<<grid_for(V * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      count_launch(3);
+      break;
+    }
+    default:
+      fail(GG_ERR_ENGINE, "no pull partitioner for this load balance");
+  }
+  GG_LAUNCH_CHECK();
+  count_launch();
+}
+
+template <class Op>
+void run_edge_only(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
+                          const OutBuilder& out) {
+  const Graph* g = rt->g;
+  cudaStream_t st = rt->stream;
+  const int dev = rt->dev;
+  if (!g->has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
+  EdgeArgs<Op> a{g->coo_view(), in, op, out, use_filter ? 1 : 0};
+  if (s.blocking) {
+    int64_t n = s.blocking_size > 0 ? s.blocking_size : default_blocking_size(*g);
+    Blocked* b = blocked_for(*const_cast<Graph*>(g), n);
+    a.coo = CooView{b->src.p, b->dst.p, g->weighted ? b->w.p : nullptr, b->E};
+    const int64_t* seg = b->seg_end.p;
+    int64_t nseg = b->nseg;
+    void* args[] = {&a, &seg, &nseg};
+    int blocks = max_coop_blocks((const void*)k_edge_blocked<Op>, 256, dev);
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_edge_blocked<Op>, blocks, 256, args, 0, st));
+  } else {
+    k_edge_only<Op><<<grid_for(g->E / 4 + 1, 256, dev, 16), 256, 0, st>>>(a);
+    GG_LAUNCH_CHECK();
+  }
+  count_launch();
+  rt->stats.edges_traversed += g->E;
+}
+
+// The output builder configuration of _OutputBuilder.__init__ (engine.py:288-309).
+template <class Op>
+std::unique_ptr<Frontier> apply_op(Runtime* rt, const Op& op, bool use_filter,
+                                          std::unique_ptr<Frontier>* input, const gg_binding& b,
+                                          bool reuse, bool collect_output) {
+  check_binding(b);
+  const Graph* g = rt->g;
+  Frontier* in = input ? input->get() : nullptr;
+  if (in && in->universe != g->V)
+    fail(GG_ERR_ENGINE, strf("frontier universe %lld does not match graph (%lld vertices)",
+                             (long long)in->universe, (long long)g->V));
+  if (in && in->retired) fail(GG_ERR_FRONTIER, "frontier was retired");
+  // hybrid_apply: s2 iff |input| > threshold * |V| (engine.py:631-632)
+  const gg_schedule* sp = &b.s1;
+  if (b.is_hybrid) {
+    int64_t size = in ? frontier_size(rt, in) : 0;
+    sp = ((double)size > b.threshold * (double)g->V) ? &b.s2 : &b.s1;
+  }
+  const gg_schedule& s = *sp;
+  rt->stats.direction_log.push_back(s.direction);
+
+  std::unique_ptr<Frontier> out;
+  if (collect_output) {
+    int repr = s.frontier_creation == GG_CREATE_FUSED
+                   ? GG_SPARSE
+                   : (s.frontier_creation == GG_CREATE_UNFUSED_BOOLMAP ? GG_BOOLMAP : GG_BITMAP);
+    out = rt->acquire(repr);
+    frontier_clear(out.get(), rt->stream);
+  }
+  OutBuilder ob = make_builder(rt, s, out.get());
+
+  // input views (engine.py:404-415, 559-565)
+  auto converted = [&](int repr) -> Frontier* { return converted_view(rt, in, repr); };
+  InView iv{};
+  iv.repr = -1;
+  if (s.load_balance == GG_LB_EDGE_ONLY) {
+    if (in) iv = (in->repr == GG_SPARSE ? converted(GG_BOOLMAP) : in)->view();
+    run_edge_only(rt, s, op, use_filter, iv, ob);
+  } else if (s.direction == GG_PUSH) {
+    int64_t n_host = g->V;
+    if (in) {
+      Frontier* sv = in->repr == GG_SPARSE ? in : converted(GG_SPARSE);
+      iv = sv->view();
+      n_host = frontier_size_raw(sv, rt->stream);
+    }
+    if (n_host > 0) run_push(rt, s, op, use_filter, iv, n_host, ob);
+  } else {
+    if (in) iv = (in->repr == s.pull_repr ? in : converted(s.pull_repr))->view();
+    run_pull(rt, s, op, use_filter, iv, ob);
+  }
+  if (rt->fused_depth == 0) rt->stats.dispatch_count += 1;
+
+  // finalize (engine.py:383-397)
+  if (out) {
+    if (s.frontier_creation == GG_CREATE_FUSED) {
+      if (ob.dedup == DEDUP_MARK_BITS || ob.dedup == DEDUP_MARK_BYTES) {
+        clear_marks(rt, out.get(), ob);
+      }
+      out->size_cache = -1;
+    } else {
+      dense_size_on_device(out.get(), rt->stream);
+      rt->stats.creation_passes += 1;
+    }
+  }
+  if (reuse && input && *input) {
+    rt->release(std::move(*input));
+    rt->stats.reused_frontiers += 1;
+  }
+  return out;
+}
+
+}  // namespace gg

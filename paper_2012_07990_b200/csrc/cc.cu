@@ -1,0 +1,89 @@
+// cc.cu — algos.cc_soman (reference algos.py:267-307) on the device.
+//
+// Round: changed = 0; edgeset.apply over all vertices with the hook functor
+// (atomic_min on label[max(la,lb)]); full pointer jumping to a fixpoint
+// (_pointer_jump, algos.py:254-264); repeat while a hook changed a label.
+// Output canonicalised to each component's minimum vertex id.
+// Fused (s0 kernel fusion): the whole loop is one cooperative launch
+// (fused.cuh).
+#include "apply.cuh"
+#include "fused.cuh"
+
+namespace gg {
+
+__global__ void k_iota_i32(int32_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)i;
+}
+
+__global__ void k_pointer_jump(int32_t* label, int64_t V, int* moved) {
+  int any = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t l = label[v], ll = label[l];
+    if (ll != l) {
+      label[v] = ll;
+      any = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, any) && lane_id() == 0) *moved = 1;
+}
+
+// first member (minimum id) of every label class, then relabel
+__global__ void k_cc_first(const int32_t* label, int64_t V, int32_t* first) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    atomicMin(first + label[v], (int32_t)v);
+}
+__global__ void k_cc_canon(const int32_t* label, const int32_t* first, int64_t V, int32_t* out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = first[label[v]];
+}
+
+void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32_t* labels_out) {
+  if (b.is_hybrid)
+    fail(GG_ERR_SCHEDULE, "label 's0:s1' of cc takes a SimpleGPUSchedule (hybrid direction "
+                          "switching applies to bfs/bc)");
+  check_binding(b);
+  DeviceGuard guard(g.dev);
+  const int64_t V = g.V;
+  const int dev = g.dev;
+  cudaStream_t st = rt.stream;
+  DevBuf<int32_t> label(V), first(V);
+  DevBuf<int> flags(2);  // [0] changed, [1] moved
+  k_iota_i32<<<grid_for(V, 256, dev), 256, 0, st>>>(label.p, V);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  if (fusion) {
+    cc_fused(rt, b.s1, label.p, flags.p);
+  } else {
+    OpHook op{label.p, flags.p};
+    int h[2] = {1, 0};
+    while (h[0]) {
+      GG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
+      rt.edge_begin();
+      apply_op(&rt, op, false, nullptr, b, false, false);
+      rt.edge_end();
+      do {  // pointer jumping to a fixpoint (host loop, not a dispatch)
+        GG_CUDA(cudaMemsetAsync(flags.p + 1, 0, sizeof(int), st));
+        k_pointer_jump<<<grid_for(V, 256, dev), 256, 0, st>>>(label.p, V, flags.p + 1);
+        GG_LAUNCH_CHECK();
+        count_launch();
+        GG_CUDA(cudaMemcpyAsync(h, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        GG_CUDA(cudaStreamSynchronize(st));
+      } while (h[1]);
+      rt.stats.rounds += 1;
+    }
+  }
+  GG_CUDA(cudaMemsetAsync(first.p, 0x7f, V * sizeof(int32_t), st));
+  k_cc_first<<<grid_for(V, 256, dev), 256, 0, st>>>(label.p, V, first.p);
+  k_cc_canon<<<grid_for(V, 256, dev), 256, 0, st>>>(label.p, first.p, V, label.p);
+  GG_LAUNCH_CHECK();
+  count_launch(2);
+  GG_CUDA(cudaMemcpyAsync(labels_out, label.p, V * sizeof(int32_t), cudaMemcpyDefault, st));
+  GG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace gg

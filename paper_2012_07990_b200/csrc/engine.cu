@@ -8,7 +8,7 @@
 //   hybrid_apply                   engine.py:622-636 (strictly greater)
 //   FrontierPool                   runtime.py:124-157
 //   VertexSubset.convert/members   frontier.py:186-265
-#include "engine.cuh"
+#include "apply.cuh"
 #include <cub/device/device_select.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -63,7 +63,7 @@ __global__ void k_popcount_bytes(const uint8_t* b, int64_t n, unsigned long long
 }
 
 // dense size into f->count (the unfused "separate materialisation pass")
-static void dense_size_on_device(Frontier* f, cudaStream_t s) {
+void dense_size_on_device(Frontier* f, cudaStream_t s) {
   GG_CUDA(cudaMemsetAsync(f->count.p, 0, sizeof(unsigned long long), s));
   if (f->repr == GG_BITMAP) {
     int64_t nw = (f->universe + 31) / 32;
@@ -322,7 +322,7 @@ void check_binding(const gg_binding& b) {
 // ---------------------------------------------------------------------------
 // Dispatch
 // ---------------------------------------------------------------------------
-static int max_coop_blocks(const void* fn, int block, int dev, size_t smem = 0) {
+int max_coop_blocks(const void* fn, int block, int dev, size_t smem) {
   int per_sm = 0;
   GG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
   if (per_sm < 1) fail(GG_ERR_CUDA, "kernel cannot be co-resident");
@@ -365,143 +365,54 @@ __global__ void k_clear_marks(const int32_t* ids, const unsigned long long* n, u
   }
 }
 
-template <class Op>
-static void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
-                     int64_t n_host, const OutBuilder& out) {
-  const Graph* g = rt->g;
+
+void strict_prefix(Runtime* rt, const InView& in, int64_t n) {
   cudaStream_t st = rt->stream;
-  PushArgs<Op> a{g->out_view(), in, op, out, use_filter ? 1 : 0, rt->scanned.p};
-  const int dev = rt->dev;
-  const int64_t work = n_host >= 0 ? n_host : g->V;
-  const int cta = rt->cfg.cta_size;
-  switch (s.load_balance) {
-    case GG_LB_VERTEX_BASED:
-      k_push_vb<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
-      break;
-    case GG_LB_WM:
-      k_push_wm<Op><<<grid_for(work * 8, 256, dev), 256, 0, st>>>(a);
-      break;
-    case GG_LB_CM:
-      k_push_cm<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
-      break;
-    case GG_LB_ETWC:
-      k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
-      break;
-    case GG_LB_STRICT: {
-      const int64_t n = n_host >= 0 ? n_host : g->V;
-      rt->prefix.alloc(n + 1);
-      DevBuf<int64_t> deg(n + 1);
-      k_degrees_of<<<grid_for(n + 1, 256, dev), 256, 0, st>>>(in, g->out_off.p, n, deg.p);
-      GG_LAUNCH_CHECK();
-      size_t temp = 0;
-      GG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, deg.p, rt->prefix.p, n + 1, st));
-      GG_CUDA(cub::DeviceScan::ExclusiveSum(rt->cub_tmp.get(temp), temp, deg.p, rt->prefix.p, n + 1, st));
-      count_launch(2);
-      k_push_strict<Op><<<grid_for(g->E / 32 + 1, 256, dev), 256, 0, st>>>(a, rt->prefix.p, 32);
-      GG_CUDA(cudaStreamSynchronize(st));  // deg freed at scope end
-      break;
-    }
-    case GG_LB_TWC: {
-      if (rt->twc_q.n < (size_t)(3 * g->V + 3)) rt->twc_q.alloc(3 * g->V + 3);
-      if (!rt->twc_cnt.p) rt->twc_cnt.alloc(3);
-      GG_CUDA(cudaMemsetAsync(rt->twc_cnt.p, 0, 3 * 8, st));
-      TwcQueues q{{rt->twc_q.p, rt->twc_q.p + g->V + 1, rt->twc_q.p + 2 * (g->V + 1)}, rt->twc_cnt.p};
-      k_twc_bin<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q, cta);
-      a.scanned = rt->scanned.p;
-      k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
-      k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
-      k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
-      count_launch(3);
-      break;
-    }
-    default:
-      fail(GG_ERR_ENGINE, "no chunker for this load balance");
-  }
+  rt->prefix.alloc(n + 1);
+  DevBuf<int64_t> deg(n + 1);
+  k_degrees_of<<<grid_for(n + 1, 256, rt->dev), 256, 0, st>>>(in, rt->g->out_view().off, n, deg.p);
+  GG_LAUNCH_CHECK();
+  size_t temp = 0;
+  GG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, deg.p, rt->prefix.p, n + 1, st));
+  GG_CUDA(cub::DeviceScan::ExclusiveSum(rt->cub_tmp.get(temp), temp, deg.p, rt->prefix.p, n + 1, st));
+  count_launch(2);
+  GG_CUDA(cudaStreamSynchronize(st));
+}
+
+void strict_spans(Runtime* rt, int64_t nspans) {
+  if (rt->spans_n == nspans) return;
+  rt->spans.alloc(nspans + 1);
+  k_strict_spans<<<grid_for(nspans + 1, 256, rt->dev), 256, 0, rt->stream>>>(
+      rt->g->in_view().off, rt->g->V, nspans, rt->spans.p);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  rt->spans_n = nspans;
+}
+
+void clear_marks(Runtime* rt, Frontier* out, const OutBuilder& ob) {
+  k_clear_marks<<<grid_for(rt->g->V, 256, rt->dev), 256, 0, rt->stream>>>(
+      out->ids.p, out->count.p, ob.mark_bits, ob.mark_bytes);
   GG_LAUNCH_CHECK();
   count_launch();
 }
 
-template <class Op>
-static void run_pull(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
-                     const OutBuilder& out) {
-  const Graph* g = rt->g;
-  cudaStream_t st = rt->stream;
-  PullArgs<Op> a{g->in_view(), in, op, out, use_filter ? 1 : 0, rt->scanned.p};
-  const int dev = rt->dev;
-  const int64_t V = g->V;
-  const int cta = rt->cfg.cta_size;
-  switch (s.load_balance) {
-    case GG_LB_VERTEX_BASED:
-      k_pull_vb<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a);
-      break;
-    case GG_LB_WM:
-      k_pull_wm<Op><<<grid_for(V * 32, 256, dev), 256, 0, st>>>(a);
-      break;
-    case GG_LB_CM:
-      k_pull_cm<Op><<<grid_for(V * 256, 256, dev), 256, 0, st>>>(a);
-      break;
-    case GG_LB_ETWC:
-      k_pull_etwc<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, cta);
-      break;
-    case GG_LB_STRICT: {
-      const int64_t nspans = std::min<int64_t>(V > 0 ? V : 1, (int64_t)sm_count(dev) * 2048);
-      if (rt->spans_n != nspans) {
-        rt->spans.alloc(nspans + 1);
-        k_strict_spans<<<grid_for(nspans + 1, 256, dev), 256, 0, st>>>(g->in_off.p, V, nspans,
-                                                                         rt->spans.p);
-        GG_LAUNCH_CHECK();
-        count_launch();
-        rt->spans_n = nspans;
-      }
-      k_pull_strict<Op><<<grid_for(nspans, 256, dev), 256, 0, st>>>(a, rt->spans.p, nspans);
-      break;
-    }
-    case GG_LB_TWC: {
-      if (rt->twc_q.n < (size_t)(3 * V + 3)) rt->twc_q.alloc(3 * V + 3);
-      if (!rt->twc_cnt.p) rt->twc_cnt.alloc(3);
-      GG_CUDA(cudaMemsetAsync(rt->twc_cnt.p, 0, 3 * 8, st));
-      TwcQueues q{{rt->twc_q.p, rt->twc_q.p + V + 1, rt->twc_q.p + 2 * (V + 1)}, rt->twc_cnt.p};
-      k_pull_twc_bin<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, q, cta);
-      k_pull_twc_thread<Op><<<grid_for(V, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
-      k_pull_twc_warp<Op><<<grid_for(V * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
-      k_pull_twc_cta<Op><<<grid_for(V * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
-      count_launch(3);
-      break;
-    }
-    default:
-      fail(GG_ERR_ENGINE, "no pull partitioner for this load balance");
-  }
-  GG_LAUNCH_CHECK();
-  count_launch();
+Frontier* converted_view(Runtime* rt, Frontier* in, int repr) {
+  rt->stats.frontier_conversions += 1;
+  if (!rt->conv || rt->conv->repr != repr)
+    rt->conv = frontier_alloc(rt->dev, rt->g->V, repr, repr == GG_SPARSE ? sparse_capacity(rt->g) : 0);
+  frontier_convert_into(rt, in, rt->conv.get());
+  return rt->conv.get();
 }
 
-template <class Op>
-static void run_edge_only(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
-                          const OutBuilder& out) {
-  const Graph* g = rt->g;
-  cudaStream_t st = rt->stream;
-  const int dev = rt->dev;
-  if (!g->has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
-  EdgeArgs<Op> a{g->coo_view(), in, op, out, use_filter ? 1 : 0};
-  if (s.blocking) {
-    int64_t n = s.blocking_size > 0 ? s.blocking_size : default_blocking_size(*g);
-    Blocked* b = blocked_for(*const_cast<Graph*>(g), n);
-    a.coo = CooView{b->src.p, b->dst.p, g->weighted ? b->w.p : nullptr, b->E};
-    const int64_t* seg = b->seg_end.p;
-    int64_t nseg = b->nseg;
-    void* args[] = {&a, &seg, &nseg};
-    int blocks = max_coop_blocks((const void*)k_edge_blocked<Op>, 256, dev);
-    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_edge_blocked<Op>, blocks, 256, args, 0, st));
-  } else {
-    k_edge_only<Op><<<grid_for(g->E / 4 + 1, 256, dev, 16), 256, 0, st>>>(a);
-    GG_LAUNCH_CHECK();
-  }
-  count_launch();
-  rt->stats.edges_traversed += g->E;
+void twc_queues(Runtime* rt, TwcQueues* q) {
+  const int64_t V = rt->g->V;
+  if (rt->twc_q.n < (size_t)(3 * V + 3)) rt->twc_q.alloc(3 * V + 3);
+  if (!rt->twc_cnt.p) rt->twc_cnt.alloc(3);
+  GG_CUDA(cudaMemsetAsync(rt->twc_cnt.p, 0, 3 * 8, rt->stream));
+  *q = TwcQueues{{rt->twc_q.p, rt->twc_q.p + V + 1, rt->twc_q.p + 2 * (V + 1)}, rt->twc_cnt.p};
 }
 
-// The output builder configuration of _OutputBuilder.__init__ (engine.py:288-309).
-static OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out) {
+OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out) {
   OutBuilder ob{};
   ob.mode = out ? s.frontier_creation : OUT_NONE;
   ob.dedup = DEDUP_NONE;
@@ -538,84 +449,6 @@ static OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out)
   return ob;
 }
 
-template <class Op>
-static std::unique_ptr<Frontier> apply_op(Runtime* rt, const Op& op, bool use_filter,
-                                          std::unique_ptr<Frontier>* input, const gg_binding& b,
-                                          bool reuse, bool collect_output) {
-  check_binding(b);
-  const Graph* g = rt->g;
-  Frontier* in = input ? input->get() : nullptr;
-  if (in && in->universe != g->V)
-    fail(GG_ERR_ENGINE, strf("frontier universe %lld does not match graph (%lld vertices)",
-                             (long long)in->universe, (long long)g->V));
-  if (in && in->retired) fail(GG_ERR_FRONTIER, "frontier was retired");
-  // hybrid_apply: s2 iff |input| > threshold * |V| (engine.py:631-632)
-  const gg_schedule* sp = &b.s1;
-  if (b.is_hybrid) {
-    int64_t size = in ? frontier_size(rt, in) : 0;
-    sp = ((double)size > b.threshold * (double)g->V) ? &b.s2 : &b.s1;
-  }
-  const gg_schedule& s = *sp;
-  rt->stats.direction_log.push_back(s.direction);
-
-  std::unique_ptr<Frontier> out;
-  if (collect_output) {
-    int repr = s.frontier_creation == GG_CREATE_FUSED
-                   ? GG_SPARSE
-                   : (s.frontier_creation == GG_CREATE_UNFUSED_BOOLMAP ? GG_BOOLMAP : GG_BITMAP);
-    out = rt->acquire(repr);
-    frontier_clear(out.get(), rt->stream);
-  }
-  OutBuilder ob = make_builder(rt, s, out.get());
-
-  // input views (engine.py:404-415, 559-565)
-  auto converted = [&](int repr) -> Frontier* {
-    rt->stats.frontier_conversions += 1;
-    if (!rt->conv || rt->conv->repr != repr)
-      rt->conv = frontier_alloc(rt->dev, g->V, repr, repr == GG_SPARSE ? sparse_capacity(g) : 0);
-    frontier_convert_into(rt, in, rt->conv.get());
-    return rt->conv.get();
-  };
-  InView iv{};
-  iv.repr = -1;
-  if (s.load_balance == GG_LB_EDGE_ONLY) {
-    if (in) iv = (in->repr == GG_SPARSE ? converted(GG_BOOLMAP) : in)->view();
-    run_edge_only(rt, s, op, use_filter, iv, ob);
-  } else if (s.direction == GG_PUSH) {
-    int64_t n_host = g->V;
-    if (in) {
-      Frontier* sv = in->repr == GG_SPARSE ? in : converted(GG_SPARSE);
-      iv = sv->view();
-      n_host = frontier_size_raw(sv, rt->stream);
-    }
-    if (n_host > 0) run_push(rt, s, op, use_filter, iv, n_host, ob);
-  } else {
-    if (in) iv = (in->repr == s.pull_repr ? in : converted(s.pull_repr))->view();
-    run_pull(rt, s, op, use_filter, iv, ob);
-  }
-  if (rt->fused_depth == 0) rt->stats.dispatch_count += 1;
-
-  // finalize (engine.py:383-397)
-  if (out) {
-    if (s.frontier_creation == GG_CREATE_FUSED) {
-      if (ob.dedup == DEDUP_MARK_BITS || ob.dedup == DEDUP_MARK_BYTES) {
-        k_clear_marks<<<grid_for(g->V, 256, rt->dev), 256, 0, rt->stream>>>(
-            out->ids.p, out->count.p, ob.mark_bits, ob.mark_bytes);
-        GG_LAUNCH_CHECK();
-        count_launch();
-      }
-      out->size_cache = -1;
-    } else {
-      dense_size_on_device(out.get(), rt->stream);
-      rt->stats.creation_passes += 1;
-    }
-  }
-  if (reuse && input && *input) {
-    rt->release(std::move(*input));
-    rt->stats.reused_frontiers += 1;
-  }
-  return out;
-}
 
 std::unique_ptr<Frontier> edgeset_apply(Runtime* rt, int udf, const gg_udf_state& st, bool use_filter,
                                         std::unique_ptr<Frontier>* input, const gg_binding& b,

@@ -27,7 +27,7 @@ struct OpBfs {
     if (atomicCAS(parent + v, -1, u) == -1) out.emit(v);
   }
   __device__ __forceinline__ Acc init() const { return -1; }
-  __device__ __forceinline__ bool visit(Acc& acc, int32_t u, uint32_t) const {
+  __device__ __forceinline__ bool visit(Acc& acc, int32_t, int32_t u, uint32_t) const {
     if (acc == -1) acc = u;
     return true;  // the first frontier in-neighbour settles v (algos.py:121-125)
   }
@@ -55,7 +55,7 @@ struct OpCount {
     atomicAdd(counts + v, 1ULL);
   }
   __device__ __forceinline__ Acc init() const { return 0; }
-  __device__ __forceinline__ bool visit(Acc& acc, int32_t, uint32_t) const { ++acc; return false; }
+  __device__ __forceinline__ bool visit(Acc& acc, int32_t, int32_t, uint32_t) const { ++acc; return false; }
   static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return a + b; }
   static __device__ __forceinline__ Acc warp_reduce(Acc a) { return warp_sum(a); }
   __device__ __forceinline__ void finish(int32_t v, const Acc& acc, const OutBuilder&) const {
@@ -73,7 +73,7 @@ struct OpEnqueue {
     out.emit(v);
   }
   __device__ __forceinline__ Acc init() const { return 0; }
-  __device__ __forceinline__ bool visit(Acc& acc, int32_t, uint32_t) const { ++acc; return false; }
+  __device__ __forceinline__ bool visit(Acc& acc, int32_t, int32_t, uint32_t) const { ++acc; return false; }
   static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return a + b; }
   static __device__ __forceinline__ Acc warp_reduce(Acc a) { return warp_sum(a); }
   __device__ __forceinline__ void finish(int32_t v, const Acc& acc, const OutBuilder& out) const {
@@ -93,7 +93,7 @@ struct OpPr {
     atomicAdd(acc + v, (double)__ldg(contrib + u));
   }
   __device__ __forceinline__ Acc init() const { return 0.0; }
-  __device__ __forceinline__ bool visit(Acc& a, int32_t u, uint32_t) const {
+  __device__ __forceinline__ bool visit(Acc& a, int32_t, int32_t u, uint32_t) const {
     a += (double)__ldg(contrib + u);
     return false;
   }
@@ -102,6 +102,134 @@ struct OpPr {
   __device__ __forceinline__ void finish(int32_t v, const Acc& a, const OutBuilder&) const {
     if (a != 0.0) acc[v] += a;
   }
+};
+
+// Connected-components hook (algos.py:283-293): atomic_min(label, hi, lo) on
+// the larger *label* (not the vertex); any direction uses the atomic form.
+struct OpHook {
+  int32_t* label;
+  int* changed;
+  using Acc = int;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ void hook(int32_t u, int32_t v) const {
+    int32_t la = *((volatile int32_t*)label + u), lb = *((volatile int32_t*)label + v);
+    if (la == lb) return;
+    int32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
+    if (atomicMin(label + hi, lo) > lo) *changed = 1;
+  }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
+    hook(u, v);
+  }
+  __device__ __forceinline__ Acc init() const { return 0; }
+  __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t) const {
+    hook(u, v);
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc) { return a; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return a; }
+  __device__ __forceinline__ void finish(int32_t, const Acc&, const OutBuilder&) const {}
+};
+
+// Delta-stepping relaxation (algos.py:233-234 -> BucketQueue.update_priority_min,
+// priority.py:59-83): atomic min on the 64-bit priority; on improvement the
+// vertex is enqueued (deduplicated) into the current bucket when its bucket
+// equals the active index, else into far.  PUSH only (algos.py:226-227).
+struct OpRelax {
+  unsigned long long* dist;
+  unsigned long long delta;
+  unsigned long long index;
+  OutBuilder cur;  // FUSED sparse + boolmap marks (per-round dedup)
+  OutBuilder far;  // FUSED sparse + boolmap marks (persistent until advance)
+  using Acc = int;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t w, const OutBuilder&) const {
+    unsigned long long du = *((volatile unsigned long long*)dist + u);
+    unsigned long long cand = du + (unsigned long long)w;
+    unsigned long long old = atomicMin(dist + v, cand);
+    if (cand < old) {
+      if (cand / delta == index) cur.emit(v);
+      else far.emit(v);
+    }
+  }
+  __device__ __forceinline__ Acc init() const { return 0; }
+  __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t w) const {
+    push(u, v, w, cur);
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc) { return a; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return a; }
+  __device__ __forceinline__ void finish(int32_t, const Acc&, const OutBuilder&) const {}
+};
+
+// Betweenness forward round (algos.py:347-365).  depth int32, sigma f64
+// (path counts; exact up to 2^53, the reference uses Python ints).
+struct BcAcc {
+  double s;
+  int found;
+};
+struct OpBcFwd {
+  int32_t* depth;
+  double* sigma;
+  int32_t level;
+  using Acc = BcAcc;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t v) const {
+    int32_t d = *((volatile int32_t*)depth + v);
+    return d == -1 || d == level + 1;
+  }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder& out) const {
+    const int32_t nl = level + 1;
+    if (atomicCAS(depth + v, -1, nl) == -1) out.emit(v);
+    if (*((volatile int32_t*)depth + v) == nl) atomicAdd(sigma + v, sigma[u]);
+  }
+  __device__ __forceinline__ Acc init() const { return {0.0, 0}; }
+  __device__ __forceinline__ bool visit(Acc& a, int32_t, int32_t u, uint32_t) const {
+    a.s += sigma[u];
+    a.found = 1;
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return {a.s + b.s, a.found | b.found}; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a.s += __shfl_xor_sync(0xffffffffu, a.s, o);
+      a.found |= __shfl_xor_sync(0xffffffffu, a.found, o);
+    }
+    return a;
+  }
+  __device__ __forceinline__ void finish(int32_t v, const Acc& a, const OutBuilder& out) const {
+    if (!a.found) return;
+    if (depth[v] == -1) {
+      depth[v] = level + 1;
+      out.emit(v);
+    }
+    sigma[v] += a.s;
+  }
+};
+
+// Betweenness backward round (algos.py:378-389), push only:
+// delta[u] += sigma[u]/sigma[v] * (1 + delta[v]) when depth[v] == depth[u]+1.
+struct OpBcBwd {
+  const int32_t* depth;
+  const double* sigma;
+  double* delta;
+  using Acc = int;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
+    if (__ldg(depth + v) == __ldg(depth + u) + 1)
+      atomicAdd(delta + u, __ldg(sigma + u) / __ldg(sigma + v) * (1.0 + delta[v]));
+  }
+  __device__ __forceinline__ Acc init() const { return 0; }
+  __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t w) const {
+    push(u, v, w, OutBuilder{});
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc) { return a; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return a; }
+  __device__ __forceinline__ void finish(int32_t, const Acc&, const OutBuilder&) const {}
 };
 
 }  // namespace gg

@@ -175,7 +175,7 @@ __device__ __forceinline__ void push_edge(const PushArgs<Op>& a, int32_t u, int6
 
 // VERTEX_BASED (engine.py:179-183): one thread per active vertex.
 template <class Op>
-__global__ void __launch_bounds__(256) k_push_vb(PushArgs<Op> a) {
+__device__ __forceinline__ void b_push_vb(PushArgs<Op> a) {
   const int64_t n = active_count(a.in, a.g.V);
   int64_t sc = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -187,12 +187,16 @@ __global__ void __launch_bounds__(256) k_push_vb(PushArgs<Op> a) {
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_vb(PushArgs<Op> a) {
+  b_push_vb<Op>(a);
+}
 
 // WM (engine.py:167-176): each warp takes 32 contiguous active vertices and
 // processes their concatenated edge lists lane-cyclically (warp prefix sum +
 // shuffle binary search to find each edge's owner).
 template <class Op>
-__global__ void __launch_bounds__(256) k_push_wm(PushArgs<Op> a) {
+__device__ __forceinline__ void b_push_wm(PushArgs<Op> a) {
   const int64_t n = active_count(a.in, a.g.V);
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -235,12 +239,16 @@ __global__ void __launch_bounds__(256) k_push_wm(PushArgs<Op> a) {
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_wm(PushArgs<Op> a) {
+  b_push_wm<Op>(a);
+}
 
 // CM (engine.py:160-164): each CTA takes blockDim contiguous active vertices
 // and processes their concatenated edges cooperatively (CTA prefix sum in
 // shared memory + binary search).
 template <class Op>
-__global__ void __launch_bounds__(256) k_push_cm(PushArgs<Op> a) {
+__device__ __forceinline__ void b_push_cm(PushArgs<Op> a) {
   __shared__ int64_t s_excl[257];
   __shared__ int64_t s_lo[256];
   __shared__ int32_t s_u[256];
@@ -282,13 +290,17 @@ __global__ void __launch_bounds__(256) k_push_cm(PushArgs<Op> a) {
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_cm(PushArgs<Op> a) {
+  b_push_cm<Op>(a);
+}
 
 // STRICT (engine.py:97-122): exact edge balance.  `prefix` is the exclusive
 // degree prefix over the active list (length n+1, computed by a device scan);
 // each thread takes a contiguous run of `per` edges and locates its first
 // owner by binary search.
 template <class Op>
-__global__ void __launch_bounds__(256) k_push_strict(PushArgs<Op> a, const int64_t* prefix,
+__device__ __forceinline__ void b_push_strict(PushArgs<Op> a, const int64_t* prefix,
                                                       int64_t per) {
   const int64_t n = active_count(a.in, a.g.V);
   const int64_t total = prefix[n];
@@ -313,6 +325,11 @@ __global__ void __launch_bounds__(256) k_push_strict(PushArgs<Op> a, const int64
   }
   if (t == 0) atomicAdd(a.scanned, (unsigned long long)total);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_strict(PushArgs<Op> a, const int64_t* prefix,
+                                                      int64_t per) {
+  b_push_strict<Op>(a, prefix, per);
+}
 
 // TWC (engine.py:125-157): global buckets by degree (> cta: CTA queue,
 // > warp: warp queue, else thread queue; strictly greater promotion).
@@ -322,7 +339,7 @@ struct TwcQueues {
 };
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_twc_bin(PushArgs<Op> a, TwcQueues q, int cta) {
+__device__ __forceinline__ void b_twc_bin(PushArgs<Op> a, TwcQueues q, int cta) {
   const int64_t n = active_count(a.in, a.g.V);
   int64_t sc = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -340,9 +357,13 @@ __global__ void __launch_bounds__(256) k_twc_bin(PushArgs<Op> a, TwcQueues q, in
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_bin(PushArgs<Op> a, TwcQueues q, int cta) {
+  b_twc_bin<Op>(a, q, cta);
+}
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_twc_thread(PushArgs<Op> a, const int32_t* qu,
+__device__ __forceinline__ void b_twc_thread(PushArgs<Op> a, const int32_t* qu,
                                                     const unsigned long long* cnt) {
   const int64_t n = (int64_t)*cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -352,9 +373,14 @@ __global__ void __launch_bounds__(256) k_twc_thread(PushArgs<Op> a, const int32_
     for (int64_t e = lo; e < hi; ++e) push_edge(a, u, e);
   }
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_thread(PushArgs<Op> a, const int32_t* qu,
+                                                    const unsigned long long* cnt) {
+  b_twc_thread<Op>(a, qu, cnt);
+}
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t* qu,
+__device__ __forceinline__ void b_twc_warp(PushArgs<Op> a, const int32_t* qu,
                                                   const unsigned long long* cnt) {
   const int64_t n = (int64_t)*cnt;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -365,9 +391,14 @@ __global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t*
     for (int64_t e = lo + lane_id(); e < hi; e += kWarp) push_edge(a, u, e);
   }
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t* qu,
+                                                  const unsigned long long* cnt) {
+  b_twc_warp<Op>(a, qu, cnt);
+}
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
+__device__ __forceinline__ void b_twc_cta(PushArgs<Op> a, const int32_t* qu,
                                                  const unsigned long long* cnt) {
   const int64_t n = (int64_t)*cnt;
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
@@ -376,6 +407,11 @@ __global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* 
     for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) push_edge(a, u, e);
   }
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
+                                                 const unsigned long long* cnt) {
+  b_twc_cta<Op>(a, qu, cnt);
+}
 
 // ETWC (engine.py:51-85, 186-193; paper Alg. 3).  Each CTA takes blockDim
 // contiguous active vertices; every vertex's range is split into a
@@ -383,12 +419,14 @@ __global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* 
 // shared memory (warp ballot + CTA prefix for slots), then the stages run in
 // order 0, 1, 2 with thread / warp / CTA cooperative processing.
 struct EtwcEntry {
-  int64_t lo, hi;
+  int64_t lo;
+  int32_t len;
   int32_t u;
+  __device__ __forceinline__ int64_t hi() const { return lo + len; }
 };
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_push_etwc(PushArgs<Op> a, int cta) {
+__device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
   __shared__ EtwcEntry s_q[3][256];
   __shared__ int s_n[3];
   const int64_t n = active_count(a.in, a.g.V);
@@ -411,8 +449,8 @@ __global__ void __launch_bounds__(256) k_push_etwc(PushArgs<Op> a, int cta) {
     int64_t e2 = (size / cta) * cta;
     int64_t e1 = ((size - e2) / kWarp) * kWarp;
     int64_t e0 = size - e2 - e1;
-    EtwcEntry c2{start, start + e2, u}, c1{start + e2, start + e2 + e1, u},
-        c0{start + e2 + e1, end, u};
+    EtwcEntry c2{start, (int32_t)e2, u}, c1{start + e2, (int32_t)e1, u},
+        c0{start + e2 + e1, (int32_t)e0, u};
     bool has[3] = {e0 > 0, e1 > 0, e2 > 0};
     const EtwcEntry* ent[3] = {&c0, &c1, &c2};
 #pragma unroll
@@ -427,21 +465,25 @@ __global__ void __launch_bounds__(256) k_push_etwc(PushArgs<Op> a, int cta) {
     // stage 0: individual threads
     for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
       EtwcEntry c = s_q[0][k];
-      for (int64_t e = c.lo; e < c.hi; ++e) push_edge(a, c.u, e);
+      for (int64_t e = c.lo; e < c.hi(); ++e) push_edge(a, c.u, e);
     }
     // stage 1: warps
     for (int k = wid; k < s_n[1]; k += nw) {
       EtwcEntry c = s_q[1][k];
-      for (int64_t e = c.lo + lane; e < c.hi; e += kWarp) push_edge(a, c.u, e);
+      for (int64_t e = c.lo + lane; e < c.hi(); e += kWarp) push_edge(a, c.u, e);
     }
     // stage 2: whole CTA
     for (int k = 0; k < s_n[2]; ++k) {
       EtwcEntry c = s_q[2][k];
-      for (int64_t e = c.lo + threadIdx.x; e < c.hi; e += blockDim.x) push_edge(a, c.u, e);
+      for (int64_t e = c.lo + threadIdx.x; e < c.hi(); e += blockDim.x) push_edge(a, c.u, e);
     }
     __syncthreads();
   }
   add_scanned(a.scanned, sc);
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_etwc(PushArgs<Op> a, int cta) {
+  b_push_etwc<Op>(a, cta);
 }
 
 // ===========================================================================
@@ -462,16 +504,16 @@ struct PullArgs {
 
 template <class Op>
 __device__ __forceinline__ bool pull_visit(const PullArgs<Op>& a, typename Op::Acc& acc,
-                                           int64_t e) {
+                                           int32_t v, int64_t e) {
   int32_t u = __ldg(a.g.nbr + e);
   if (!a.in.member(u)) return false;
   uint32_t w = a.g.w ? __ldg(a.g.w + e) : 0u;
-  return a.op.visit(acc, u, w);
+  return a.op.visit(acc, v, u, w);
 }
 
 // VERTEX_BASED: thread per destination (early exit when the op says so).
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_vb(PullArgs<Op> a) {
+__device__ __forceinline__ void b_pull_vb(PullArgs<Op> a) {
   int64_t sc = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.g.V;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -480,20 +522,24 @@ __global__ void __launch_bounds__(256) k_pull_vb(PullArgs<Op> a) {
     sc += hi - lo;
     typename Op::Acc acc = a.op.init();
     for (int64_t e = lo; e < hi; ++e)
-      if (pull_visit(a, acc, e)) break;
+      if (pull_visit(a, acc, (int32_t)v, e)) break;
     a.op.finish((int32_t)v, acc, a.out);
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_vb(PullArgs<Op> a) {
+  b_pull_vb<Op>(a);
+}
 
 // Warp-cooperative reduction of one destination's in-range [lo, hi).
 template <class Op>
-__device__ __forceinline__ typename Op::Acc pull_warp_range(const PullArgs<Op>& a, int64_t lo,
-                                                            int64_t hi) {
+__device__ __forceinline__ typename Op::Acc pull_warp_range(const PullArgs<Op>& a, int32_t v,
+                                                            int64_t lo, int64_t hi) {
   typename Op::Acc acc = a.op.init();
   for (int64_t e0 = lo; e0 < hi; e0 += kWarp) {
     bool stop = false;
-    if (e0 + lane_id() < hi) stop = pull_visit(a, acc, e0 + lane_id());
+    if (e0 + lane_id() < hi) stop = pull_visit(a, acc, v, e0 + lane_id());
     if (Op::kEarlyExit && __any_sync(0xffffffffu, stop)) break;
   }
   return Op::warp_reduce(acc);
@@ -502,7 +548,7 @@ __device__ __forceinline__ typename Op::Acc pull_warp_range(const PullArgs<Op>& 
 // WM: warps take contiguous destination chunks; each destination's in-list
 // is reduced by the whole warp.
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_wm(PullArgs<Op> a) {
+__device__ __forceinline__ void b_pull_wm(PullArgs<Op> a) {
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t chunk = (a.g.V + nwarps - 1) / nwarps;
@@ -511,10 +557,14 @@ __global__ void __launch_bounds__(256) k_pull_wm(PullArgs<Op> a) {
     if (a.use_filter && !a.op.filter((int32_t)v)) continue;
     int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
     if (lane_id() == 0) sc += hi - lo;
-    typename Op::Acc acc = pull_warp_range(a, lo, hi);
+    typename Op::Acc acc = pull_warp_range(a, (int32_t)v, lo, hi);
     if (lane_id() == 0) a.op.finish((int32_t)v, acc, a.out);
   }
   add_scanned(a.scanned, sc);
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_wm(PullArgs<Op> a) {
+  b_pull_wm<Op>(a);
 }
 
 // Block-wide reduction helper (accumulators are tiny PODs).
@@ -534,7 +584,7 @@ __device__ __forceinline__ typename Op::Acc block_reduce(typename Op::Acc acc) {
 // CM: CTAs take contiguous destination chunks; each destination's in-list is
 // reduced by the whole CTA.
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_cm(PullArgs<Op> a) {
+__device__ __forceinline__ void b_pull_cm(PullArgs<Op> a) {
   __shared__ int s_keep;
   const int64_t chunk = (a.g.V + gridDim.x - 1) / gridDim.x;
   int64_t sc = 0;
@@ -547,18 +597,22 @@ __global__ void __launch_bounds__(256) k_pull_cm(PullArgs<Op> a) {
     int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
     if (threadIdx.x == 0) sc += hi - lo;
     typename Op::Acc acc = a.op.init();
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, e);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, (int32_t)v, e);
     acc = block_reduce<Op>(acc);
     if (threadIdx.x == 0) a.op.finish((int32_t)v, acc, a.out);
   }
   add_scanned(a.scanned, sc);
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_cm(PullArgs<Op> a) {
+  b_pull_cm<Op>(a);
 }
 
 // STRICT (engine.py:216-225): edge-balanced destination spans snapped to
 // vertex boundaries (each destination keeps one owner).  `span_start[t]` is
 // the first destination of span t (length nspans+1), computed on the device.
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_strict(PullArgs<Op> a, const int64_t* span_start,
+__device__ __forceinline__ void b_pull_strict(PullArgs<Op> a, const int64_t* span_start,
                                                      int64_t nspans) {
   int64_t sc = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nspans;
@@ -569,17 +623,22 @@ __global__ void __launch_bounds__(256) k_pull_strict(PullArgs<Op> a, const int64
       sc += hi - lo;
       typename Op::Acc acc = a.op.init();
       for (int64_t e = lo; e < hi; ++e)
-        if (pull_visit(a, acc, e)) break;
+        if (pull_visit(a, acc, (int32_t)v, e)) break;
       a.op.finish((int32_t)v, acc, a.out);
     }
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_strict(PullArgs<Op> a, const int64_t* span_start,
+                                                     int64_t nspans) {
+  b_pull_strict<Op>(a, span_start, nspans);
+}
 
 // TWC pull (engine.py:249-251): destinations binned by in-degree; the three
 // consumers reuse thread / warp / CTA reduction.
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_twc_bin(PullArgs<Op> a, TwcQueues q, int cta) {
+__device__ __forceinline__ void b_pull_twc_bin(PullArgs<Op> a, TwcQueues q, int cta) {
   int64_t sc = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.g.V;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -596,9 +655,13 @@ __global__ void __launch_bounds__(256) k_pull_twc_bin(PullArgs<Op> a, TwcQueues 
   }
   add_scanned(a.scanned, sc);
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_bin(PullArgs<Op> a, TwcQueues q, int cta) {
+  b_pull_twc_bin<Op>(a, q, cta);
+}
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_twc_thread(PullArgs<Op> a, const int32_t* qv,
+__device__ __forceinline__ void b_pull_twc_thread(PullArgs<Op> a, const int32_t* qv,
                                                          const unsigned long long* cnt) {
   const int64_t n = (int64_t)*cnt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -607,36 +670,51 @@ __global__ void __launch_bounds__(256) k_pull_twc_thread(PullArgs<Op> a, const i
     int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
     typename Op::Acc acc = a.op.init();
     for (int64_t e = lo; e < hi; ++e)
-      if (pull_visit(a, acc, e)) break;
+      if (pull_visit(a, acc, v, e)) break;
     a.op.finish(v, acc, a.out);
   }
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_thread(PullArgs<Op> a, const int32_t* qv,
+                                                         const unsigned long long* cnt) {
+  b_pull_twc_thread<Op>(a, qv, cnt);
+}
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_twc_warp(PullArgs<Op> a, const int32_t* qv,
+__device__ __forceinline__ void b_pull_twc_warp(PullArgs<Op> a, const int32_t* qv,
                                                        const unsigned long long* cnt) {
   const int64_t n = (int64_t)*cnt;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n; i += nwarps) {
     int32_t v = qv[i];
-    typename Op::Acc acc = pull_warp_range(a, __ldg(a.g.off + v), __ldg(a.g.off + v + 1));
+    typename Op::Acc acc = pull_warp_range(a, v, __ldg(a.g.off + v), __ldg(a.g.off + v + 1));
     if (lane_id() == 0) a.op.finish(v, acc, a.out);
   }
 }
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_warp(PullArgs<Op> a, const int32_t* qv,
+                                                       const unsigned long long* cnt) {
+  b_pull_twc_warp<Op>(a, qv, cnt);
+}
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_twc_cta(PullArgs<Op> a, const int32_t* qv,
+__device__ __forceinline__ void b_pull_twc_cta(PullArgs<Op> a, const int32_t* qv,
                                                       const unsigned long long* cnt) {
   const int64_t n = (int64_t)*cnt;
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     int32_t v = qv[i];
     int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
     typename Op::Acc acc = a.op.init();
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, e);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, v, e);
     acc = block_reduce<Op>(acc);
     if (threadIdx.x == 0) a.op.finish(v, acc, a.out);
   }
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_twc_cta(PullArgs<Op> a, const int32_t* qv,
+                                                      const unsigned long long* cnt) {
+  b_pull_twc_cta<Op>(a, qv, cnt);
 }
 
 // ETWC pull (engine.py:252-255): chunked in-ranges stay inside one CTA.  Each
@@ -644,7 +722,7 @@ __global__ void __launch_bounds__(256) k_pull_twc_cta(PullArgs<Op> a, const int3
 // kept per destination slot in shared memory and combined by the owner
 // thread, which then performs the single owner write.
 template <class Op>
-__global__ void __launch_bounds__(256) k_pull_etwc(PullArgs<Op> a, int cta) {
+__device__ __forceinline__ void b_pull_etwc(PullArgs<Op> a, int cta) {
   __shared__ EtwcEntry s_q[3][256];
   __shared__ int s_slot[3][256];  // queue entry -> destination slot
   __shared__ typename Op::Acc s_part[3][256];
@@ -669,8 +747,8 @@ __global__ void __launch_bounds__(256) k_pull_etwc(PullArgs<Op> a, int cta) {
     int64_t e2 = (size / cta) * cta;
     int64_t e1 = ((size - e2) / kWarp) * kWarp;
     int64_t e0 = size - e2 - e1;
-    EtwcEntry c[3] = {{start + e2 + e1, end, (int32_t)v}, {start + e2, start + e2 + e1, (int32_t)v},
-                      {start, start + e2, (int32_t)v}};
+    EtwcEntry c[3] = {{start + e2 + e1, (int32_t)e0, (int32_t)v}, {start + e2, (int32_t)e1, (int32_t)v},
+                      {start, (int32_t)e2, (int32_t)v}};
     bool has[3] = {e0 > 0, e1 > 0, e2 > 0};
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -687,19 +765,19 @@ __global__ void __launch_bounds__(256) k_pull_etwc(PullArgs<Op> a, int cta) {
     for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
       EtwcEntry ce = s_q[0][k];
       typename Op::Acc acc = a.op.init();
-      for (int64_t e = ce.lo; e < ce.hi; ++e)
-        if (pull_visit(a, acc, e)) break;
+      for (int64_t e = ce.lo; e < ce.hi(); ++e)
+        if (pull_visit(a, acc, ce.u, e)) break;
       s_part[0][s_slot[0][k]] = acc;
     }
     for (int k = wid; k < s_n[1]; k += nw) {
       EtwcEntry ce = s_q[1][k];
-      typename Op::Acc acc = pull_warp_range(a, ce.lo, ce.hi);
+      typename Op::Acc acc = pull_warp_range(a, ce.u, ce.lo, ce.hi());
       if (lane == 0) s_part[1][s_slot[1][k]] = acc;
     }
     for (int k = 0; k < s_n[2]; ++k) {
       EtwcEntry ce = s_q[2][k];
       typename Op::Acc acc = a.op.init();
-      for (int64_t e = ce.lo + threadIdx.x; e < ce.hi; e += blockDim.x) pull_visit(a, acc, e);
+      for (int64_t e = ce.lo + threadIdx.x; e < ce.hi(); e += blockDim.x) pull_visit(a, acc, ce.u, e);
       acc = block_reduce<Op>(acc);
       if (threadIdx.x == 0) s_part[2][s_slot[2][k]] = acc;
     }
@@ -712,6 +790,10 @@ __global__ void __launch_bounds__(256) k_pull_etwc(PullArgs<Op> a, int cta) {
     __syncthreads();
   }
   add_scanned(a.scanned, sc);
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_pull_etwc(PullArgs<Op> a, int cta) {
+  b_pull_etwc<Op>(a, cta);
 }
 
 // ===========================================================================
@@ -760,16 +842,20 @@ __device__ __forceinline__ void edge_range(const EdgeArgs<Op>& a, int64_t lo, in
 }
 
 template <class Op>
-__global__ void __launch_bounds__(256) k_edge_only(EdgeArgs<Op> a) {
+__device__ __forceinline__ void b_edge_only(EdgeArgs<Op> a) {
   edge_range(a, 0, a.coo.E, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
              (int64_t)gridDim.x * blockDim.x);
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_edge_only(EdgeArgs<Op> a) {
+  b_edge_only<Op>(a);
 }
 
 // EdgeBlocking Alg. 2 (blocking.py:116-186): segments in order, the whole
 // grid cooperates on one segment, grid barrier between segments.  Launched
 // cooperatively (one dispatch).
 template <class Op>
-__global__ void __launch_bounds__(256) k_edge_blocked(EdgeArgs<Op> a, const int64_t* seg_end,
+__device__ __forceinline__ void b_edge_blocked(EdgeArgs<Op> a, const int64_t* seg_end,
                                                       int64_t nseg) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -781,6 +867,11 @@ __global__ void __launch_bounds__(256) k_edge_blocked(EdgeArgs<Op> a, const int6
     lo = hi;
     grid.sync();
   }
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_edge_blocked(EdgeArgs<Op> a, const int64_t* seg_end,
+                                                      int64_t nseg) {
+  b_edge_blocked<Op>(a, seg_end, nseg);
 }
 
 }  // namespace gg
