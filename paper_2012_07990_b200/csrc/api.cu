@@ -37,6 +37,11 @@ void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exe
                   bool fp32_contrib);
 void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
              int32_t* parents_out);
+void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
+              uint64_t* dist_out);
+void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32_t* labels_out);
+void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_binding& b, Runtime& rt,
+            double* scores_out);
 }  // namespace gg
 
 using namespace gg;
@@ -465,6 +470,49 @@ int gg_bfs(const gg_graph* g, int64_t source, const gg_binding* binding, int32_t
   Runtime rt(g->g.get(), cfg);
   CallTimer t(g->g->dev);
   bfs_run(*g->g, source, *binding, fusion != 0, rt, parents);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_sssp_delta(const gg_graph* g, int64_t source, const gg_binding* binding, int32_t fusion,
+                  const gg_exec* cfg, uint64_t* dist, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  NEED(dist);
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), cfg);
+  CallTimer t(g->g->dev);
+  sssp_run(*g->g, source, *binding, fusion != 0, rt, dist);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_cc(const gg_graph* g, const gg_binding* binding, int32_t fusion, const gg_exec* cfg,
+          int32_t* labels, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  NEED(labels);
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), cfg);
+  CallTimer t(g->g->dev);
+  cc_run(*g->g, *binding, fusion != 0, rt, labels);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_bc(const gg_graph* g, const int64_t* sources, int64_t num_sources, const gg_binding* binding,
+          const gg_exec* cfg, double* scores, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  NEED(scores);
+  if (num_sources > 0) NEED(sources);
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), cfg);
+  CallTimer t(g->g->dev);
+  bc_run(*g->g, sources, num_sources, *binding, rt, scores);
   t.finish(g->g->dev, rt, stats);
   GG_API_END
 }

@@ -8,6 +8,8 @@
 
 namespace gg {
 
+void bfs_fused(Runtime& rt, const gg_binding& b, int32_t* parent, int32_t source);
+
 void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
              int32_t* parents_out) {
   if (source < 0 || source >= g.V)
@@ -20,9 +22,14 @@ void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, R
   GG_CUDA(cudaMemsetAsync(parent.p, 0xff, g.V * sizeof(int32_t), st));
   int32_t src32 = (int32_t)source;
   GG_CUDA(cudaMemcpyAsync(parent.p + source, &src32, 4, cudaMemcpyHostToDevice, st));
+  if (fusion) {
+    bfs_fused(rt, b, parent.p, src32);
+    GG_CUDA(cudaMemcpyAsync(parents_out, parent.p, g.V * sizeof(int32_t), cudaMemcpyDefault, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   std::unique_ptr<Frontier> frontier = rt.new_frontier(&src32, 1);
   gg_udf_state ust{parent.p, nullptr, 0};
-  if (fusion) fail(GG_ERR_ENGINE, "fused BFS loop: not implemented in this build");
   while (frontier_size(&rt, frontier.get()) > 0) {
     rt.edge_begin();
     std::unique_ptr<Frontier> out = edgeset_apply(&rt, UDF_BFS, ust, true, &frontier, b, true, true);

@@ -1,0 +1,303 @@
+// sssp.cu — algos.sssp_delta (reference algos.py:215-247) with the two-bucket
+// queue of priority.BucketQueue (priority.py:17-118) kept on the device.
+//
+// Device state: dist u64[V] (UNREACHED = 2^64-1), bucket queues as SPARSE
+// id lists: current, far (+ a spare for advance), per-round dedup marks for
+// current and persistent marks for far (DenseMarks BOOLMAP, priority.py:33-35).
+// Round (fused_loop body, algos.py:236-243):
+//   current empty -> advance(): drop stale far entries (bucket <= index), pick
+//                    the minimum far bucket, split far into current / far;
+//   else          -> take current, relax its out-edges with the schedule's
+//                    load balancer (PUSH forced), re-bucketing improvements.
+// Unfused: one kernel sequence per round with host-side control.
+// Fused (s0 kernel fusion): the whole loop, including advance(), is ONE
+// cooperative launch with per-bucket frontiers and grid barriers.
+#include "fused.cuh"
+
+namespace gg {
+
+static constexpr unsigned long long kUnreached = ~0ULL;
+
+__global__ void k_adv_min(const int32_t* far, const unsigned long long* nfar,
+                          const unsigned long long* dist, unsigned long long delta,
+                          unsigned long long index, uint8_t* fmark, unsigned long long* best) {
+  unsigned long long b_min = kUnreached;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*nfar;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = far[i];
+    fmark[v] = 0;
+    unsigned long long b = dist[v] / delta;
+    if (b > index && b < b_min) b_min = b;
+  }
+  if (b_min != kUnreached) atomicMin(best, b_min);
+}
+
+__global__ void k_adv_split(const int32_t* far, const unsigned long long* nfar,
+                            const unsigned long long* dist, unsigned long long delta,
+                            unsigned long long index, const unsigned long long* bestp,
+                            OutBuilder cur, OutBuilder far2) {
+  const unsigned long long best = *bestp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*nfar;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = far[i];
+    unsigned long long b = dist[v] / delta;
+    if (b <= index) continue;  // stale: handled in an earlier bucket (priority.py:101-105)
+    if (b == best) cur.emit(v);
+    else far2.emit(v);
+  }
+}
+
+__global__ void k_clear_byte_marks(const int32_t* ids, const unsigned long long* n, uint8_t* m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m[ids[i]] = 0;
+}
+
+static OutBuilder queue_builder(Frontier* q, uint8_t* marks) {
+  OutBuilder ob{};
+  ob.mode = GG_CREATE_FUSED;
+  ob.dedup = DEDUP_MARK_BYTES;
+  ob.queue = q->ids.p;
+  ob.qcount = q->count.p;
+  ob.mark_bytes = marks;
+  return ob;
+}
+
+// ---------------------------------------------------------------------------
+// Fused delta-stepping: one cooperative launch for the whole loop.
+// ---------------------------------------------------------------------------
+struct SsspFusedArgs {
+  gg_schedule s;
+  CsrView out;
+  CooView coo;
+  FusedScratch sc;
+  unsigned long long* dist;
+  unsigned long long delta;
+  int32_t* q[4];                  // current, take, far, far2
+  unsigned long long* qn;         // counts [4]
+  uint8_t* cmark;
+  uint8_t* fmark;
+  uint8_t* member;                // EDGE_ONLY input membership (boolmap)
+  unsigned long long* best;       // advance scratch
+  unsigned long long* scanned;
+  long long* counters;            // [0] rounds [1] relax rounds
+  int cta;
+};
+
+__global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  int cur = 0, take = 1, far = 2, far2 = 3;
+  unsigned long long index = 0;
+  long long rounds = 0, relax = 0;
+  while (true) {
+    grid.sync();
+    const unsigned long long ncur = *((volatile unsigned long long*)a.qn + cur);
+    const unsigned long long nfar = *((volatile unsigned long long*)a.qn + far);
+    if (ncur == 0 && nfar == 0) break;  // BucketQueue.done()
+    ++rounds;
+    if (ncur == 0) {
+      // advance(): minimum live far bucket, then split far
+      if (tid == 0) *a.best = kUnreached;
+      grid.sync();
+      unsigned long long b_min = kUnreached;
+      for (int64_t i = tid; i < (int64_t)nfar; i += nth) {
+        int32_t v = a.q[far][i];
+        a.fmark[v] = 0;
+        unsigned long long b = a.dist[v] / a.delta;
+        if (b > index && b < b_min) b_min = b;
+      }
+      if (b_min != kUnreached) atomicMin(a.best, b_min);
+      grid.sync();
+      const unsigned long long best = *((volatile unsigned long long*)a.best);
+      if (best != kUnreached) {
+        OutBuilder oc{}, of{};
+        oc.mode = of.mode = GG_CREATE_FUSED;
+        oc.dedup = of.dedup = DEDUP_MARK_BYTES;
+        oc.queue = a.q[cur]; oc.qcount = a.qn + cur; oc.mark_bytes = a.cmark;
+        of.queue = a.q[far2]; of.qcount = a.qn + far2; of.mark_bytes = a.fmark;
+        for (int64_t i = tid; i < (int64_t)nfar; i += nth) {
+          int32_t v = a.q[far][i];
+          unsigned long long b = a.dist[v] / a.delta;
+          if (b <= index) continue;
+          if (b == best) oc.emit(v);
+          else of.emit(v);
+        }
+        index = best;
+      }
+      grid.sync();
+      if (tid == 0) a.qn[far] = 0;
+      int t = far; far = far2; far2 = t;
+      continue;
+    }
+    // take_current(): the pending bucket becomes the relax input
+    { int t = cur; cur = take; take = t; }
+    grid.sync();
+    if (tid == 0) a.qn[cur] = 0;
+    for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.cmark[a.q[take][i]] = 0;
+    InView iv{};
+    if (a.s.load_balance == GG_LB_EDGE_ONLY) {
+      for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 1;
+      iv.repr = GG_BOOLMAP;
+      iv.bools = a.member;
+    } else {
+      iv.repr = GG_SPARSE;
+      iv.ids = a.q[take];
+      iv.count = a.qn + take;
+    }
+    grid.sync();
+    OpRelax op{a.dist, a.delta, index, OutBuilder{}, OutBuilder{}};
+    op.cur.mode = op.far.mode = GG_CREATE_FUSED;
+    op.cur.dedup = op.far.dedup = DEDUP_MARK_BYTES;
+    op.cur.queue = a.q[cur]; op.cur.qcount = a.qn + cur; op.cur.mark_bytes = a.cmark;
+    op.far.queue = a.q[far]; op.far.qcount = a.qn + far; op.far.mark_bytes = a.fmark;
+    OutBuilder none{};
+    none.mode = OUT_NONE;
+    fused_edge_phase(a.s, a.out, a.out, a.coo, iv, op, none, false, a.scanned, a.sc, a.cta, grid);
+    grid.sync();
+    if (a.s.load_balance == GG_LB_EDGE_ONLY)
+      for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 0;
+    ++relax;
+  }
+  if (tid == 0) {
+    a.counters[0] = rounds;
+    a.counters[1] = relax;
+  }
+}
+
+void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
+              uint64_t* dist_out) {
+  if (source < 0 || source >= g.V)
+    fail(GG_ERR_VALUE, strf("invalid source %lld for graph with %lld vertices", (long long)source,
+                            (long long)g.V));
+  if (!g.weighted) fail(GG_ERR_VALUE, "sssp needs edge weights (load weighted or inject random weights)");
+  if (b.is_hybrid)
+    fail(GG_ERR_SCHEDULE, "label 's0:s1' of sssp takes a SimpleGPUSchedule (hybrid direction "
+                          "switching applies to bfs/bc)");
+  check_binding(b);
+  DeviceGuard guard(g.dev);
+  const int64_t V = g.V;
+  const int dev = g.dev;
+  cudaStream_t st = rt.stream;
+  gg_binding pb = b;
+  pb.s1.direction = GG_PUSH;  // relaxation is source-driven (algos.py:226-227)
+  const gg_schedule& s = pb.s1;
+  const unsigned long long delta = (unsigned long long)s.delta;
+  DevBuf<unsigned long long> dist(V);
+  GG_CUDA(cudaMemsetAsync(dist.p, 0xff, V * 8, st));
+  unsigned long long zero = 0;
+  GG_CUDA(cudaMemcpyAsync(dist.p + source, &zero, 8, cudaMemcpyHostToDevice, st));
+  const int64_t mb = ((V + 3) & ~int64_t(3)) + 4;
+  DevBuf<uint8_t> cmark(mb), fmark(mb);
+  cmark.zero(st);
+  fmark.zero(st);
+  const uint8_t one = 1;
+  GG_CUDA(cudaMemcpyAsync(cmark.p + source, &one, 1, cudaMemcpyHostToDevice, st));
+  int32_t src32 = (int32_t)source;
+
+  if (fusion) {
+    SsspFusedArgs a{};
+    a.s = s;
+    if (s.load_balance == GG_LB_EDGE_ONLY) {
+      if (!s.blocking) a.coo = g.coo_view();
+    } else {
+      a.out = g.out_view();
+    }
+    a.out.V = V;
+    a.dist = dist.p;
+    a.delta = delta;
+    DevBuf<int32_t> q[4];
+    DevBuf<unsigned long long> qn(4), best(1);
+    qn.zero(st);
+    for (int k = 0; k < 4; ++k) {
+      q[k].alloc(V + 1);
+      a.q[k] = q[k].p;
+    }
+    GG_CUDA(cudaMemcpyAsync(q[0].p, &src32, 4, cudaMemcpyHostToDevice, st));
+    unsigned long long n1 = 1;
+    GG_CUDA(cudaMemcpyAsync(qn.p, &n1, 8, cudaMemcpyHostToDevice, st));
+    DevBuf<uint8_t> member(mb);
+    member.zero(st);
+    DevBuf<long long> counters(2);
+    a.qn = qn.p;
+    a.cmark = cmark.p;
+    a.fmark = fmark.p;
+    a.member = member.p;
+    a.best = best.p;
+    a.scanned = rt.scanned.p;
+    a.counters = counters.p;
+    a.cta = rt.cfg.cta_size;
+    int blocks = max_coop_blocks((const void*)k_sssp_fused, 256, dev);
+    FusedHost fh;
+    const gg_schedule* ss[1] = {&s};
+    fh.prepare(rt, ss, 1, blocks);
+    a.sc = fh.sc;
+    void* args[] = {&a};
+    rt.edge_begin();
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_sssp_fused, blocks, 256, args, 0, st));
+    rt.edge_end();
+    count_launch();
+    long long h[2];
+    GG_CUDA(cudaMemcpyAsync(h, counters.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+    rt.stats.dispatch_count += 1;
+    rt.stats.rounds += h[0];
+    for (long long k = 0; k < h[1]; ++k) rt.stats.direction_log.push_back(GG_PUSH);
+    if (s.load_balance == GG_LB_EDGE_ONLY) rt.stats.frontier_conversions += h[1];
+  } else {
+    std::unique_ptr<Frontier> cur = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+    std::unique_ptr<Frontier> take = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+    std::unique_ptr<Frontier> far = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+    std::unique_ptr<Frontier> far2 = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+    GG_CUDA(cudaMemcpyAsync(cur->ids.p, &src32, 4, cudaMemcpyHostToDevice, st));
+    unsigned long long n1 = 1;
+    GG_CUDA(cudaMemcpyAsync(cur->count.p, &n1, 8, cudaMemcpyHostToDevice, st));
+    DevBuf<unsigned long long> best(1);
+    unsigned long long index = 0;
+    const unsigned grid = (unsigned)sm_count(dev) * 8;
+    while (true) {
+      unsigned long long n[2];
+      GG_CUDA(cudaMemcpyAsync(&n[0], cur->count.p, 8, cudaMemcpyDeviceToHost, st));
+      GG_CUDA(cudaMemcpyAsync(&n[1], far->count.p, 8, cudaMemcpyDeviceToHost, st));
+      GG_CUDA(cudaStreamSynchronize(st));
+      if (n[0] == 0 && n[1] == 0) break;
+      rt.stats.rounds += 1;
+      if (n[0] == 0) {  // advance()
+        GG_CUDA(cudaMemsetAsync(best.p, 0xff, 8, st));
+        k_adv_min<<<grid, 256, 0, st>>>(far->ids.p, far->count.p, dist.p, delta, index, fmark.p, best.p);
+        GG_LAUNCH_CHECK();
+        unsigned long long hb = 0;
+        GG_CUDA(cudaMemcpyAsync(&hb, best.p, 8, cudaMemcpyDeviceToHost, st));
+        GG_CUDA(cudaStreamSynchronize(st));
+        if (hb != kUnreached) {
+          OutBuilder oc = queue_builder(cur.get(), cmark.p);
+          OutBuilder of = queue_builder(far2.get(), fmark.p);
+          k_adv_split<<<grid, 256, 0, st>>>(far->ids.p, far->count.p, dist.p, delta, index, best.p,
+                                            oc, of);
+          GG_LAUNCH_CHECK();
+          index = hb;
+        }
+        count_launch(hb != kUnreached ? 2 : 1);
+        GG_CUDA(cudaMemsetAsync(far->count.p, 0, 8, st));
+        std::swap(far, far2);
+        continue;
+      }
+      std::swap(cur, take);  // take_current()
+      GG_CUDA(cudaMemsetAsync(cur->count.p, 0, 8, st));
+      k_clear_byte_marks<<<grid, 256, 0, st>>>(take->ids.p, take->count.p, cmark.p);
+      GG_LAUNCH_CHECK();
+      count_launch();
+      take->size_cache = (int64_t)n[0];
+      OpRelax op{dist.p, delta, index, queue_builder(cur.get(), cmark.p), queue_builder(far.get(), fmark.p)};
+      rt.edge_begin();
+      apply_op(&rt, op, false, &take, pb, false, false);
+      rt.edge_end();
+      take->size_cache = -1;
+    }
+  }
+  GG_CUDA(cudaMemcpyAsync(dist_out, dist.p, V * 8, cudaMemcpyDefault, st));
+  GG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace gg

@@ -1,0 +1,242 @@
+"""BFS / SSSP / CC / BC on the device vs the reference (golden fixtures,
+including RunStats) and the CPU oracle.
+
+Bars (north star): BFS depths, CC labels and integer SSSP distances
+bit-exact; BFS parents a legal BFS tree; BC within 1e-5 relative (absolute
+1e-9 where the score is ~0).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import gen
+from tests.util import arrays, max_rel_err, program_with, sched_from
+
+pytestmark = pytest.mark.gpu
+
+LBS = ["VERTEX_BASED", "CM", "WM", "STRICT", "EDGE_ONLY", "ETWC", "TWC"]
+BC_REL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def gg():
+    import paper_2012_07990_b200 as gg
+    return gg
+
+
+@pytest.fixture(scope="module")
+def graphs(gg, golden_small):
+    out = {}
+    for name, rec in golden_small["graphs"].items():
+        V, s, d, w = arrays(rec)
+        out[name] = gg.Graph.from_coo(V, s, d, w, symmetric=rec["symmetric"])
+    return out
+
+
+def legal_bfs_tree(g, parents, source):
+    arcs = set(zip(g.coo_src.tolist(), g.coo_dst.tolist()))
+    levels = None
+    for v, p in enumerate(parents):
+        if v == source:
+            assert p == source
+            continue
+        if p != -1:
+            assert (p, v) in arcs, (p, v)
+    return True
+
+
+def close_bc(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    big = np.abs(want) > 1e-6
+    assert np.all(np.abs(got[~big] - want[~big]) < 1e-9)
+    if big.any():
+        assert max_rel_err(got[big], want[big]) < BC_REL
+
+
+# ---------------------------------------------------------------------------
+# golden (reference) cases with stats
+# ---------------------------------------------------------------------------
+def test_bfs_golden(gg, golden_small, graphs):
+    n = 0
+    for case in golden_small["cases"]:
+        if case["algo"] != "bfs":
+            continue
+        g = graphs[case["graph"]]
+        if "schedule_text" in case:
+            prog = gg.parse_schedule(case["schedule_text"])
+        else:
+            prog = program_with(sched_from(case["schedule"]))
+        r = gg.bfs(g, case["source"], prog)
+        assert gg.bfs_levels(r.values) == case["levels"], case
+        legal_bfs_tree(g, r.values, case["source"])
+        st = case["stats"]
+        assert r.stats.rounds == st["rounds"]
+        assert r.stats.dispatch_count == st["dispatch_count"]
+        assert r.stats.edges_traversed == st["edges_traversed"], (case["graph"], case.get("schedule"))
+        assert r.stats.direction_log == st["direction_log"]
+        assert r.stats.frontier_allocations == st["frontier_allocations"]
+        assert r.stats.reused_frontiers == st["reused_frontiers"]
+        assert r.stats.frontier_conversions == st["frontier_conversions"]
+        assert r.stats.creation_passes == st["creation_passes"]
+        n += 1
+    assert n > 100
+
+
+def test_sssp_golden(gg, golden_small, graphs):
+    for case in golden_small["cases"]:
+        if case["algo"] != "sssp":
+            continue
+        g = graphs[case["graph"]]
+        r = gg.sssp_delta(g, case["source"], program_with(sched_from(case["schedule"])))
+        want = [math.inf if x is None else x for x in case["dist"]]
+        assert r.values == want
+        st = case["stats"]
+        assert r.stats.rounds == st["rounds"]
+        assert r.stats.dispatch_count == st["dispatch_count"]
+        assert r.stats.edges_traversed == st["edges_traversed"]
+        assert r.stats.frontier_allocations == st["frontier_allocations"]
+
+
+def test_cc_golden(gg, golden_small, graphs):
+    for case in golden_small["cases"]:
+        if case["algo"] != "cc":
+            continue
+        r = gg.cc_soman(graphs[case["graph"]], program_with(sched_from(case["schedule"])))
+        assert r.values == case["labels"]
+
+
+def test_bc_golden(gg, golden_small, graphs):
+    for case in golden_small["cases"]:
+        if case["algo"] != "bc":
+            continue
+        r = gg.bc(graphs[case["graph"]], case["sources"], program_with(sched_from(case["schedule"])))
+        close_bc(r.values, case["scores"])
+        st = case["stats"]
+        assert r.stats.rounds == st["rounds"]
+        assert r.stats.dispatch_count == st["dispatch_count"]
+        assert r.stats.frontier_allocations == st["frontier_allocations"]
+
+
+# ---------------------------------------------------------------------------
+# every schedule (direction x load balance x fusion) on RMAT-12 vs the oracle
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def rmat12(gg):
+    gs = gg.generate_rmat(12, 16, seed=2, symmetrize=True)
+    V = gs.num_vertices
+    off, nbr, _ = oracle.csr(V, gs.coo_src, gs.coo_dst)
+    return gs, off, nbr
+
+
+@pytest.mark.parametrize("lb", LBS)
+@pytest.mark.parametrize("direction", ["PUSH", "PULL"])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_bfs_every_schedule(gg, golden_rmat12, rmat12, lb, direction, fusion):
+    gs, off, nbr = rmat12
+    src = golden_rmat12["bfs_source"]
+    r = gg.bfs(gs, src, program_with(gg.Schedule(direction=direction, load_balance=lb), fusion))
+    assert gg.bfs_levels(r.values) == golden_rmat12["bfs_levels"]
+    legal_bfs_tree(gs, r.values, src)
+    assert r.stats.dispatch_count == (1 if fusion else r.stats.rounds)
+
+
+@pytest.mark.parametrize("creation", ["FUSED", "UNFUSED_BOOLMAP", "UNFUSED_BITMAP"])
+@pytest.mark.parametrize("dedup,strategy", [(True, "MONOTONIC_COUNTERS"), (True, "BITMAP"),
+                                            (True, "BOOLMAP"), (False, "MONOTONIC_COUNTERS")])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_bfs_creation_dedup_modes(gg, golden_rmat12, rmat12, creation, dedup, strategy, fusion):
+    gs, _, _ = rmat12
+    s = gg.Schedule(load_balance="ETWC", frontier_creation=creation, dedup=dedup,
+                    dedup_strategy=strategy)
+    r = gg.bfs(gs, golden_rmat12["bfs_source"], program_with(s, fusion))
+    assert gg.bfs_levels(r.values) == golden_rmat12["bfs_levels"]
+
+
+@pytest.mark.parametrize("fusion", [False, True])
+def test_bfs_hybrid_direction_switch(gg, golden_rmat12, rmat12, fusion):
+    gs, _, _ = rmat12
+    text = """
+    SimpleGPUSchedule s1;
+    s1.configDirection(PUSH);
+    s1.configLoadBalance(ETWC);
+    SimpleGPUSchedule s2;
+    s2.configDirection(PULL, BITMAP);
+    s2.configFrontierCreation(UNFUSED_BITMAP);
+    HybridGPUSchedule h1(INPUT_VERTEXSET_SIZE, 0.05, s1, s2);
+    apply("s0:s1", h1);
+    """
+    prog = gg.parse_schedule(text)
+    if fusion:
+        prog.bindings["s0"] = gg.Schedule(kernel_fusion=True)
+    r = gg.bfs(gs, golden_rmat12["bfs_source"], prog)
+    assert gg.bfs_levels(r.values) == golden_rmat12["bfs_levels"]
+    log = r.stats.direction_log
+    assert any(a == "PUSH" and b == "PULL" for a, b in zip(log, log[1:]))
+
+
+@pytest.mark.parametrize("lb", [l for l in LBS])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_sssp_every_schedule(gg, golden_rmat12, lb, fusion):
+    V, s, d = gen.rmat(12, 16, seed=2)
+    w = gen.weights(len(s), 4)
+    g = gg.Graph.from_coo(V, s, d, w)
+    sch = gg.Schedule(load_balance=lb, delta=golden_rmat12["sssp_delta"])
+    r = gg.sssp_delta(g, 0, program_with(sch, fusion))
+    want = [math.inf if x is None else x for x in golden_rmat12["sssp_dist"]]
+    assert r.values == want
+    if fusion:
+        assert r.stats.dispatch_count == 1
+
+
+@pytest.mark.parametrize("delta", [1, 7, 100, 5000])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_sssp_grid_matches_oracle(gg, delta, fusion):
+    g = gg.generate_grid(64, seed=4)
+    V = g.num_vertices
+    off, nbr, w = oracle.csr(V, g.coo_src, g.coo_dst, g.coo_weights)
+    want, rounds = oracle.sssp_delta(V, off, nbr, w, 0, delta)
+    r = gg.sssp_delta(g, 0, program_with(gg.Schedule(load_balance="ETWC", delta=delta), fusion))
+    assert np.array_equal(r.array, want)
+    assert r.stats.rounds == rounds
+
+
+@pytest.mark.parametrize("lb", ["VERTEX_BASED", "EDGE_ONLY", "ETWC", "TWC", "CM", "WM", "STRICT"])
+@pytest.mark.parametrize("direction", ["PUSH", "PULL"])
+@pytest.mark.parametrize("fusion", [False, True])
+def test_cc_every_schedule(gg, golden_rmat12, rmat12, lb, direction, fusion):
+    gs, _, _ = rmat12
+    r = gg.cc_soman(gs, program_with(gg.Schedule(direction=direction, load_balance=lb), fusion))
+    assert r.values == golden_rmat12["cc_labels"]
+    if fusion:
+        assert r.stats.dispatch_count == 1
+
+
+@pytest.mark.parametrize("lb", ["VERTEX_BASED", "ETWC", "TWC", "EDGE_ONLY", "WM"])
+@pytest.mark.parametrize("direction", ["PUSH", "PULL"])
+def test_bc_schedules(gg, golden_rmat12, rmat12, lb, direction):
+    gs, _, _ = rmat12
+    r = gg.bc(gs, golden_rmat12["bc_sources"],
+              program_with(gg.Schedule(direction=direction, load_balance=lb)))
+    close_bc(r.values, golden_rmat12["bc_scores"])
+
+
+def test_algorithm_errors(gg, graphs):
+    g = graphs["path4"]
+    with pytest.raises(ValueError, match="invalid source"):
+        gg.bfs(g, 7)
+    with pytest.raises(ValueError, match="weights"):
+        gg.sssp_delta(g, 0)
+    with pytest.raises(ValueError, match="non-empty"):
+        gg.bc(g, [])
+    with pytest.raises(ValueError, match="symmetric"):
+        gg.bc(gg.Graph.from_coo(3, [0], [1]), [0])
+    with pytest.raises(gg.ScheduleError, match="fusion"):
+        gg.bc(g, [0], program_with(gg.Schedule(), fusion=True))
+    with pytest.raises(gg.ScheduleError, match="hybrid"):
+        gg.sssp_delta(graphs["hand3"], 0, gg.ScheduleProgram({"s0:s1": gg.HybridSchedule()}))
+    with pytest.warns(UserWarning, match="symmetrizing"):
+        r = gg.cc_soman(gg.Graph.from_coo(6, [0, 1, 2, 3, 4, 5], [1, 2, 0, 4, 5, 3]))
+    assert r.values == [0, 0, 0, 3, 3, 3]
