@@ -42,6 +42,8 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
 void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32_t* labels_out);
 void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_binding& b, Runtime& rt,
             double* scores_out);
+int64_t pagerank_dist_run(gg_comm* c, const Graph& g, int64_t max_iters, double tol, double damping,
+                          double* ranks_out, Runtime& rt);
 }  // namespace gg
 
 using namespace gg;
@@ -513,6 +515,20 @@ int gg_bc(const gg_graph* g, const int64_t* sources, int64_t num_sources, const 
   Runtime rt(g->g.get(), cfg);
   CallTimer t(g->g->dev);
   bc_run(*g->g, sources, num_sources, *binding, rt, scores);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_pagerank_dist(gg_comm* c, const gg_graph* g, int64_t max_iters, double tolerance,
+                     double damping, double* ranks, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(c);
+  NEED(g);
+  NEED(ranks);
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), nullptr);
+  CallTimer t(g->g->dev);
+  pagerank_dist_run(c, *g->g, max_iters, tolerance, damping, ranks, rt);
   t.finish(g->g->dev, rt, stats);
   GG_API_END
 }

@@ -1,0 +1,67 @@
+"""Multi-GPU PageRank: 1-D destination partition over NCCL.
+
+One process per GPU (torchrun).  ``Comm.create`` exchanges the NCCL unique id
+through ``torch.distributed`` (any backend; gloo works for the exchange) and
+builds a libgg communicator on this rank's device; ``pagerank_dist`` runs the
+partitioned PageRank (csrc/dist.cu) and returns the full rank vector on every
+rank.  ``partition_bounds`` is the host statement of the partition rule the
+device uses (destination ranges balanced by in-edge count).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .runtime import RunStats
+
+
+def partition_bounds(in_offsets, nranks):
+    """bounds[r] = first v with in_off[v] >= r*E/P (bounds[0]=0, bounds[P]=V)."""
+    off = np.asarray(in_offsets, dtype=np.int64)
+    V = len(off) - 1
+    E = int(off[-1])
+    b = [0]
+    for r in range(1, nranks):
+        target = (E * r) // nranks
+        b.append(int(np.searchsorted(off[:V], target, side="left")))
+    b.append(V)
+    return b
+
+
+class Comm:
+    def __init__(self, handle, rank, world, device):
+        self._h = handle
+        self.rank, self.world, self.device = rank, world, device
+
+    @classmethod
+    def create(cls, rank, world, device, group=None):
+        import torch
+        import torch.distributed as dist
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _lib.call("gg_nccl_unique_id", uid)
+        if world > 1:
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda(device)
+            dist.broadcast(t, 0, group=group)
+            uid = (C.c_char * 128)(*t.cpu().numpy().tobytes())
+        h = C.c_void_p()
+        _lib.call("gg_comm_init", device, world, rank, uid, C.byref(h))
+        return cls(h, rank, world, device)
+
+    def close(self):
+        if self._h is not None:
+            _lib.load().gg_comm_destroy(self._h)
+            self._h = None
+
+
+def pagerank_dist(comm, g, max_iters=100, tolerance=1e-9, damping=0.85, out=None):
+    ranks = out if out is not None else np.empty(g.num_vertices, np.float64)
+    st = _lib.new_stats()
+    _lib.call("gg_pagerank_dist", comm._h, g.handle, int(max_iters), float(tolerance),
+              float(damping), _lib.ptr(ranks), C.byref(st))
+    return ranks, RunStats.from_pod(st)
