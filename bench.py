@@ -202,15 +202,14 @@ def main():
     V, E = g.num_vertices, g.num_edges
     sch = gg.Schedule(**SCHEDULES[args.schedule])
     prog = gg.ScheduleProgram({"s0:s1": sch})
-    prep_ms = 0.0
-    if sch.blocking:
-        bg_t = time.perf_counter()
-        import ctypes as C
-        from paper_2012_07990_b200 import _lib
-        h, pm = C.c_void_p(), C.c_double()
-        n = gg.default_blocking_size(g)
-        _lib.call("gg_block_edges", g.handle, n, C.byref(h), C.byref(pm))
-        prep_ms = pm.value
+    import ctypes as C
+    from paper_2012_07990_b200 import _lib
+    from paper_2012_07990_b200.engine import binding_pod
+    pm = C.c_double()
+    pod = binding_pod(sch)
+    _lib.call("gg_pagerank_prepare", g.handle, C.byref(pod), 1 if args.fp32_contrib else 0,
+              C.byref(pm))
+    prep_ms = pm.value
     ranks = torch.empty(V, dtype=torch.float64, device="cuda")
 
     def step():

@@ -210,6 +210,12 @@ int gg_pagerank(const gg_graph* g, const gg_binding* binding, int32_t fusion,
                 double* ranks, gg_stats* stats);                              /* algos.py:163 */
 /* gg_pagerank with the contribution vector stored as f32 (accumulation stays
  * f64); halves the bytes of the random gathers on the largest graphs. */
+/* Build (and cache on the graph) whatever layout the bound PageRank schedule
+ * uses -- the EdgeBlocking source-segment layout for EDGE_ONLY+BLOCKED, the
+ * pull plan for PULL -- and report its preprocessing time, which the
+ * reference's CLI also times apart from the runs (cli.py:178-192). */
+int gg_pagerank_prepare(const gg_graph* g, const gg_binding* binding, int32_t fp32_contrib,
+                        double* prep_ms);
 int gg_pagerank_ex(const gg_graph* g, const gg_binding* binding, int32_t fusion,
                    const gg_exec* cfg, int64_t max_iters, double tolerance, double damping,
                    int32_t fp32_contrib, double* ranks, gg_stats* stats);

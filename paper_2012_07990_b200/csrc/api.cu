@@ -44,6 +44,10 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
             double* scores_out);
 int64_t pagerank_dist_run(gg_comm* c, const Graph& g, int64_t max_iters, double tol, double damping,
                           double* ranks_out, Runtime& rt);
+double pr_block_prep_ms(const Graph& g, int64_t blocking_size, int ct_bytes);
+inline void pr_block_prep(const Graph& g, int64_t blocking_size, int ct_bytes) {
+  pr_block_prep_ms(g, blocking_size, ct_bytes);
+}
 }  // namespace gg
 
 using namespace gg;
@@ -530,6 +534,30 @@ int gg_pagerank_dist(gg_comm* c, const gg_graph* g, int64_t max_iters, double to
   CallTimer t(g->g->dev);
   pagerank_dist_run(c, *g->g, max_iters, tolerance, damping, ranks, rt);
   t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_pagerank_prepare(const gg_graph* g, const gg_binding* binding, int32_t fp32_contrib,
+                        double* prep_ms) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  DeviceGuard guard(g->g->dev);
+  check_binding(*binding);
+  double t0 = now_ms();
+  const gg_schedule& s = binding->s1;
+  if (s.load_balance == GG_LB_EDGE_ONLY && s.blocking) {
+    pr_block_prep(*g->g, s.blocking_size, fp32_contrib ? 4 : 8);
+  } else if (s.load_balance == GG_LB_EDGE_ONLY) {
+    g->g->out_view();
+  } else if (s.direction == GG_PULL) {
+    g->g->out_view();
+    g->g->in_view();
+  } else {
+    g->g->out_view();
+  }
+  GG_CUDA(cudaDeviceSynchronize());
+  if (prep_ms) *prep_ms = now_ms() - t0;
   GG_API_END
 }
 

@@ -45,10 +45,14 @@ __global__ void __launch_bounds__(256) k_cc_fused(CcFusedArgs a) {
       }
       if (__any_sync(0xffffffffu, any) && lane_id() == 0) atomicOr(a.flags + 1, 1);
       grid.sync();
-      if (!*((volatile int*)a.flags + 1)) break;
+      const int moved = *((volatile int*)a.flags + 1);
+      grid.sync();  // every thread has read the flag before thread 0 resets it
+      if (!moved) break;
     }
     ++rounds;
-    if (!*((volatile int*)a.flags)) break;
+    const int changed = *((volatile int*)a.flags);
+    grid.sync();
+    if (!changed) break;
   }
   if (tid == 0) a.flags[2] = rounds;
 }

@@ -285,6 +285,10 @@ static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, cons
   GG_CUDA(cudaStreamSynchronize(st));
 }
 
+template <class CT>
+int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int64_t max_iters,
+                         double tol, double damping, double* ranks_out, Runtime& rt);
+
 void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
                   int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
                   bool fp32_contrib) {
@@ -294,6 +298,13 @@ void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exe
                           "switching applies to bfs/bc)");
   check_binding(b);
   DeviceGuard guard(g.dev);
+  if (b.s1.load_balance == GG_LB_EDGE_ONLY && b.s1.blocking) {
+    if (fp32_contrib)
+      pagerank_blocked<float>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt);
+    else
+      pagerank_blocked<double>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt);
+    return;
+  }
   if (fp32_contrib)
     pagerank_impl<float>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt);
   else

@@ -156,8 +156,13 @@ __device__ __forceinline__ void pr_finish(const PrPullArgs<CT>& a, int32_t v, do
   else dm += nv;
 }
 
-template <class CT>
-__device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t it, double* s_acc_all) {
+// MODE 0: whole rows, finish in place.  MODE 1 (cold EdgeBlocking segment):
+// add row sums into acc (== hubsum).  MODE 2 (hot, final segment): finish
+// with sum + acc and reset acc.  Hub pieces always add into hubsum.
+template <class CT, int MODE = 0>
+__device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t it, double* s_acc_all,
+                                               int64_t c_begin = 0, int64_t c_end = -1) {
+  if (c_end < 0) c_end = a.nchunks;
   const int lane = lane_id();
   const int wib = threadIdx.x >> 5;
   double* s_acc = s_acc_all + wib * 32;
@@ -166,7 +171,7 @@ __device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t 
   double l1 = 0, dm = 0;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = warp; c < a.nchunks; c += nwarps) {
+  for (int64_t c = c_begin + warp; c < c_end; c += nwarps) {
     const int64_t vr = c * 32 + lane;
     const int64_t lo = __ldg(a.voff + vr);
     const int64_t deg = __ldg(a.voff + vr + 1) - lo;
@@ -209,16 +214,27 @@ __device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t 
     const double sum = s_acc[lane];
     __syncwarp();
     if (owner >= 0) {
-      pr_finish(a, owner, sum, base, l1, dm);
+      if (MODE == 1) {
+        if (sum != 0.0) a.hubsum[owner] += sum;
+      } else {
+        double s = sum;
+        if (MODE == 2) {
+          s += a.hubsum[owner];
+          a.hubsum[owner] = 0.0;
+        }
+        pr_finish(a, owner, s, base, l1, dm);
+      }
     } else if (owner != INT32_MIN && sum != 0.0) {
       atomicAdd(a.hubsum + ~owner, sum);
     }
   }
-  l1 = block_sum(l1);
-  dm = block_sum(dm);
-  if (threadIdx.x == 0) {
-    if (l1 != 0.0) atomicAdd(a.scal + 2 * it + 1, l1);
-    if (dm != 0.0) atomicAdd(a.scal + 2 * (it + 1), dm);
+  if (MODE != 1) {
+    l1 = block_sum(l1);
+    dm = block_sum(dm);
+    if (threadIdx.x == 0) {
+      if (l1 != 0.0) atomicAdd(a.scal + 2 * it + 1, l1);
+      if (dm != 0.0) atomicAdd(a.scal + 2 * (it + 1), dm);
+    }
   }
 }
 
@@ -246,6 +262,13 @@ template <class CT>
 __global__ void __launch_bounds__(256) k_pr_pull(PrPullArgs<CT> a, int64_t it) {
   __shared__ double s_acc[8 * 32];
   pr_pull_chunks(a, it, s_acc);
+}
+
+template <class CT, int MODE>
+__global__ void __launch_bounds__(256) k_pr_seg(PrPullArgs<CT> a, int64_t it, int64_t c_begin,
+                                                int64_t c_end) {
+  __shared__ double s_acc[8 * 32];
+  pr_pull_chunks<CT, MODE>(a, it, s_acc, c_begin, c_end);
 }
 
 template <class CT>
