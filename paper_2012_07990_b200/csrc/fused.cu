@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(256) k_bfs_fused(BfsFusedArgs a) {
     else need = s.pull_repr;
     InView iv{};
     iv.repr = need;
+    iv.coherent = 1;
     if (need == cur_repr) {
       iv.ids = in.ids; iv.count = in.count; iv.bits = in.bits; iv.bools = in.bools;
     } else {

@@ -181,7 +181,7 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   L->V = V;
   L->E = E;
   L->ct_bytes = ct_bytes;
-  L->hub_t = 4096;
+  L->hub_t = kPieceEdges;
   const int nvb = nbits((uint64_t)(V > 1 ? V - 1 : 1));
   const int kb = nbits((uint64_t)(L->K > 1 ? L->K - 1 : 1));
   if (32 + nvb + kb > 64) fail(GG_ERR_VALUE, "EdgeBlocking layout: too many segments for this graph");
@@ -380,6 +380,7 @@ static __global__ void __launch_bounds__(256) k_prb_fused(PrPullArgs<CT> a, CT* 
                                                           int64_t* iters_out) {
   __shared__ double s_acc[8 * 32];
   cg::grid_group grid = cg::this_grid();
+  a.coherent = 1;
   int64_t it = 0;
   double l1 = INFINITY;
   while (!(it >= max_iters || l1 < tol)) {

@@ -33,6 +33,10 @@ __device__ __forceinline__ double block_sum(double v) {
 // contrib.  Hub pieces add their partial sums into hubsum[row] (f64 atomic)
 // and the hub pass finishes those rows.  No per-edge atomics.
 // ---------------------------------------------------------------------------
+// Longest virtual row: a warp owns 32 consecutive virtual rows, so a chunk
+// carries at most 32 * kPieceEdges edges (bounded warp work -> no stragglers).
+constexpr int64_t kPieceEdges = 64;
+
 struct PullPlan {
   int64_t hub_t = 0, nvrows = 0, nhubs = 0, lo = 0, hi = 0;
   DevBuf<int64_t> voff;    // nvrows + 1
@@ -142,6 +146,7 @@ struct PrPullArgs {
   double* scal;
   int64_t V;
   double damping;
+  int coherent = 0;  // fused loops re-read contrib written earlier in the same launch
 };
 
 // finish one destination: fused vertex pass (algos.py:192-198 + :184-189)
@@ -198,7 +203,10 @@ __device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t 
       const int64_t exj = __shfl_sync(0xffffffffu, excl, j);
       double val = 0.0;
       const bool live = k < total;
-      if (live) val = (double)__ldg(a.contrib + __ldg(a.nbr + loj + (k - exj)));
+      if (live) {
+        const int32_t u = __ldg(a.nbr + loj + (k - exj));
+        val = (double)(a.coherent ? __ldcg(a.contrib + u) : __ldg(a.contrib + u));
+      }
       // segmented inclusive scan over runs of equal owner lane j
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -283,6 +291,7 @@ __global__ void __launch_bounds__(256) k_pr_pull_fused(PrPullArgs<CT> a, CT* c0,
                                                        int64_t* iters_out) {
   __shared__ double s_acc[8 * 32];
   cg::grid_group grid = cg::this_grid();
+  a.coherent = 1;
   int64_t it = 0;
   double l1 = INFINITY;
   while (!(it >= max_iters || l1 < tol)) {

@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
     if (tid == 0) a.qn[cur] = 0;
     for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.cmark[a.q[take][i]] = 0;
     InView iv{};
+    iv.coherent = 1;
     if (a.s.load_balance == GG_LB_EDGE_ONLY) {
       for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 1;
       iv.repr = GG_BOOLMAP;

@@ -45,11 +45,13 @@ struct InView {
   const unsigned long long* count;
   const uint32_t* bits;
   const uint8_t* bools;
+  int coherent = 0;  // fused loops: membership written earlier in the same launch
 
   __device__ __forceinline__ int64_t size() const { return (int64_t)*count; }
   __device__ __forceinline__ bool member(int32_t u) const {
-    if (repr == GG_BITMAP) return (__ldg(bits + (u >> 5)) >> (u & 31)) & 1u;
-    if (repr == GG_BOOLMAP) return __ldg(bools + u) != 0;
+    if (repr == GG_BITMAP)
+      return ((coherent ? __ldcg(bits + (u >> 5)) : __ldg(bits + (u >> 5))) >> (u & 31)) & 1u;
+    if (repr == GG_BOOLMAP) return (coherent ? __ldcg(bools + u) : __ldg(bools + u)) != 0;
     return true;  // all active
   }
 };
