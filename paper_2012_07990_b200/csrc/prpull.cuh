@@ -191,33 +191,48 @@ __device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t 
     const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
     s_acc[lane] = 0.0;
     __syncwarp();
-    for (int64_t k0 = 0; k0 < total; k0 += 32) {
-      const int64_t k = k0 + lane;
-      int j = 0;
+    // kU strides of 32 edges per step: all index loads, then all gathers,
+    // then the reductions -- kU*32 independent gathers in flight per warp.
+    constexpr int kU = 4;
+    for (int64_t k0 = 0; k0 < total; k0 += 32 * kU) {
+      int jv[kU];
+      int32_t uv[kU];
+      double val[kU];
 #pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        int64_t em = __shfl_sync(0xffffffffu, excl, j + step);
-        if (em <= k) j += step;
-      }
-      const int64_t loj = __shfl_sync(0xffffffffu, lo, j);
-      const int64_t exj = __shfl_sync(0xffffffffu, excl, j);
-      double val = 0.0;
-      const bool live = k < total;
-      if (live) {
-        const int32_t u = __ldg(a.nbr + loj + (k - exj));
-        val = (double)(a.coherent ? __ldcg(a.contrib + u) : __ldg(a.contrib + u));
-      }
-      // segmented inclusive scan over runs of equal owner lane j
+      for (int q = 0; q < kU; ++q) {
+        const int64_t k = k0 + q * 32 + lane;
+        int j = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        double t = __shfl_up_sync(0xffffffffu, val, o);
-        int jj = __shfl_up_sync(0xffffffffu, j, o);
-        if (lane >= o && jj == j) val += t;
+        for (int step = 16; step >= 1; step >>= 1) {
+          int64_t em = __shfl_sync(0xffffffffu, excl, j + step);
+          if (em <= k) j += step;
+        }
+        const int64_t loj = __shfl_sync(0xffffffffu, lo, j);
+        const int64_t exj = __shfl_sync(0xffffffffu, excl, j);
+        jv[q] = j;
+        uv[q] = k < total ? __ldg(a.nbr + loj + (k - exj)) : -1;
       }
-      const int jn = __shfl_down_sync(0xffffffffu, j, 1);
-      const bool tail = live && (lane == 31 || jn != j || k + 1 >= total);
-      if (tail) s_acc[j] += val;
-      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kU; ++q)
+        val[q] = uv[q] >= 0 ? (double)(a.coherent ? __ldcg(a.contrib + uv[q]) : __ldg(a.contrib + uv[q]))
+                            : 0.0;
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const int64_t k = k0 + q * 32 + lane;
+        const int j = jv[q];
+        double v = val[q];
+        // segmented inclusive scan over runs of equal owner lane j
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          double t = __shfl_up_sync(0xffffffffu, v, o);
+          int jj = __shfl_up_sync(0xffffffffu, j, o);
+          if (lane >= o && jj == j) v += t;
+        }
+        const int jn = __shfl_down_sync(0xffffffffu, j, 1);
+        const bool tail = k < total && (lane == 31 || jn != j || k + 1 >= total);
+        if (tail) s_acc[j] += v;
+        __syncwarp();
+      }
     }
     const double sum = s_acc[lane];
     __syncwarp();
