@@ -31,6 +31,7 @@ struct Graph {
   std::map<int64_t, std::unique_ptr<Blocked>> blocked;
   std::shared_ptr<PullPlan> pull_plan;
   std::shared_ptr<void> pr_block;  // PageRank EdgeBlocking layout (prblock.cu)
+  std::shared_ptr<void> pr_tiles;  // merge-path tile plan over CSR-in (pagerank.cu)
   // CSR views are built on first use (a schedule that only streams the COO
   // never pays for the transpose); guarded by view_mu.
   bool has_out = false, has_in = false;

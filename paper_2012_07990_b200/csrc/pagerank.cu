@@ -13,7 +13,10 @@
 // no host synchronisation is needed between rounds unless tolerance > 0.
 // The vertex pass fuses: rank update, L1, next dangling mass, next contrib
 // and the acc reset (one read of acc/rank/deg, one write of rank/contrib/acc).
-#include "prpull.cuh"
+#include "prtile.cuh"
+#include "apply.cuh"
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 namespace gg {
 
@@ -199,6 +202,165 @@ static int64_t pagerank_pull_wm(const Graph& g, bool fusion, int64_t max_iters, 
   return it;
 }
 
+// ---------------------------------------------------------------------------
+// PULL + STRICT: exact edge balance as merge-path tiles over CSR-in (rows
+// split by a tile boundary are combined through an f64 add and finished in
+// the crossing pass).  Same kernel as the EdgeBlocking path, minus the
+// blocking (no renumbering, no source segments): the ablation baseline.
+// ---------------------------------------------------------------------------
+static __global__ void k_tile_starts_g(const int64_t* roff, int64_t nrows, int64_t ntiles, int64_t* trow,
+                                       int64_t* tedge) {
+  const int64_t ne = roff[nrows];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = t * (int64_t)kTile;
+    if (d > nrows + ne) d = nrows + ne;
+    int64_t lo = 0, hi = nrows;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (roff[mid + 1] + mid < d) lo = mid + 1; else hi = mid;
+    }
+    trow[t] = lo;
+    tedge[t] = d - lo;
+  }
+}
+
+static TilePlan* csr_tiles_for(const Graph& gc) {
+  Graph& g = const_cast<Graph&>(gc);
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.pr_tiles) return static_cast<TilePlan*>(g.pr_tiles.get());
+  CsrView in = g.in_view();
+  const int dev = g.dev;
+  auto tp = std::make_shared<TilePlan>();
+  tp->nrows = g.V;
+  tp->ntiles = (g.V + g.E + kTile - 1) / kTile;
+  tp->tile_row.alloc(tp->ntiles + 1);
+  tp->tile_edge.alloc(tp->ntiles + 1);
+  k_tile_starts_g<<<grid_for(tp->ntiles + 1, 256, dev), 256>>>(in.off, g.V, tp->ntiles, tp->tile_row.p,
+                                                                tp->tile_edge.p);
+  GG_LAUNCH_CHECK();
+  DevBuf<uint8_t> mark(g.V + 1);
+  mark.zero();
+  if (tp->ntiles > 1)
+    k_mark_cross<<<grid_for(tp->ntiles, 256, dev), 256>>>(in.off, tp->tile_row.p, tp->tile_edge.p,
+                                                          tp->ntiles, 0, g.V, mark.p);
+  GG_LAUNCH_CHECK();
+  tp->cross.alloc(g.V + 1);
+  DevBuf<unsigned long long> n(1);
+  cub::CountingInputIterator<int32_t> it((int32_t)0);
+  size_t temp = 0;
+  GG_CUDA(cub::DeviceSelect::Flagged(nullptr, temp, it, mark.p, tp->cross.p, n.p, g.V));
+  DevBuf<uint8_t> tb(temp);
+  GG_CUDA(cub::DeviceSelect::Flagged(tb.p, temp, it, mark.p, tp->cross.p, n.p, g.V));
+  unsigned long long h = 0;
+  GG_CUDA(cudaMemcpy(&h, n.p, 8, cudaMemcpyDeviceToHost));
+  tp->ncross = (int64_t)h;
+  g.pr_tiles = tp;
+  return tp.get();
+}
+
+template <class CT>
+static __global__ void __launch_bounds__(kTileThreads) k_pr_tiles_fused(TileArgs<CT> a, CT* c0, CT* c1,
+                                                                        const int32_t* cross,
+                                                                        int64_t ncross, int64_t max_iters,
+                                                                        double tol, int64_t* iters_out) {
+  __shared__ double s_val[kTile];
+  __shared__ int32_t s_rend[kTile + 1];
+  __shared__ double s_rowsum[kTile + 1];
+  cg::grid_group grid = cg::this_grid();
+  a.coherent = 1;
+  int64_t it = 0;
+  double l1 = INFINITY;
+  while (!(it >= max_iters || l1 < tol)) {
+    a.contrib = (it & 1) ? c1 : c0;
+    a.contrib_next = (it & 1) ? c0 : c1;
+    pr_tiles<CT, 0>(a, it, s_val, s_rend, s_rowsum);
+    grid.sync();
+    pr_crossing(a, it, cross, ncross);
+    grid.sync();
+    l1 = *((volatile double*)a.scal + 2 * it + 1);
+    ++it;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *iters_out = it;
+}
+
+template <class CT>
+static int64_t pagerank_pull_tiles(const Graph& g, bool fusion, int64_t max_iters, double tol,
+                                   double damping, double* rank, CT* contrib0, double* scal,
+                                   Runtime& rt) {
+  const int64_t V = g.V;
+  const int dev = g.dev;
+  cudaStream_t st = rt.stream;
+  TilePlan* tp = csr_tiles_for(g);
+  CsrView in = g.in_view();
+  DevBuf<CT> contrib1(V);
+  DevBuf<double> hubsum(V);
+  hubsum.zero(st);
+  DevBuf<int32_t> outdeg(V);
+  k_outdeg<<<grid_for(V, 256, dev), 256, 0, st>>>(g.out_view().off, V, outdeg.p);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  TileArgs<CT> a{};
+  a.roff = in.off;
+  a.owner = nullptr;
+  a.row_base = 0;
+  a.src = in.nbr;
+  a.tile_row = tp->tile_row.p;
+  a.tile_edge = tp->tile_edge.p;
+  a.ntiles = tp->ntiles;
+  a.rank = rank;
+  a.outdeg = outdeg.p;
+  a.acc = hubsum.p;
+  a.hubsum = hubsum.p;
+  a.scal = scal;
+  a.V = V;
+  a.damping = damping;
+  int64_t it = 0;
+  if (!fusion) {
+    double l1 = INFINITY;
+    const unsigned grid = (unsigned)sm_count(dev) * 5;
+    const unsigned cgrid = grid_for(tp->ncross, 256, dev);
+    while (!(it >= max_iters || l1 < tol)) {
+      a.contrib = (it & 1) ? contrib1.p : contrib0;
+      a.contrib_next = (it & 1) ? contrib0 : contrib1.p;
+      rt.edge_begin();
+      k_pr_tiles<CT, 0><<<grid, kTileThreads, 0, st>>>(a, it);
+      if (tp->ncross) k_pr_crossing<CT><<<cgrid, 256, 0, st>>>(a, it, tp->cross.p, tp->ncross);
+      rt.edge_end();
+      GG_LAUNCH_CHECK();
+      count_launch(tp->ncross ? 2 : 1);
+      rt.stats.dispatch_count += 1;
+      rt.stats.direction_log.push_back(GG_PULL);
+      ++it;
+      if (tol > 0.0) {
+        GG_CUDA(cudaMemcpyAsync(&l1, scal + 2 * (it - 1) + 1, 8, cudaMemcpyDeviceToHost, st));
+        GG_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+  } else {
+    DevBuf<int64_t> iters(1);
+    int blocks = max_coop_blocks((const void*)k_pr_tiles_fused<CT>, kTileThreads, dev);
+    CT* c0 = contrib0;
+    CT* c1 = contrib1.p;
+    const int32_t* cr = tp->cross.p;
+    int64_t nc = tp->ncross;
+    int64_t* ip = iters.p;
+    void* args[] = {&a, &c0, &c1, &cr, &nc, &max_iters, &tol, &ip};
+    rt.edge_begin();
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_pr_tiles_fused<CT>, blocks, kTileThreads, args, 0,
+                                        st));
+    rt.edge_end();
+    count_launch();
+    GG_CUDA(cudaMemcpyAsync(&it, iters.p, 8, cudaMemcpyDeviceToHost, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+    rt.stats.dispatch_count += 1;
+    for (int64_t k = 0; k < it; ++k) rt.stats.direction_log.push_back(GG_PULL);
+  }
+  rt.stats.rounds += it;
+  rt.stats.edges_traversed += it * g.E;
+  return it;
+}
+
 template <class CT>
 static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
                           int64_t max_iters, double tol, double damping, double* ranks_out,
@@ -218,6 +380,8 @@ static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, cons
   int64_t it = 0;
   if (s.direction == GG_PULL && s.load_balance == GG_LB_WM) {
     pagerank_pull_wm<CT>(g, fusion, max_iters, tol, damping, rank.p, contrib.p, scal.p, rt);
+  } else if (s.direction == GG_PULL && s.load_balance == GG_LB_STRICT) {
+    pagerank_pull_tiles<CT>(g, fusion, max_iters, tol, damping, rank.p, contrib.p, scal.p, rt);
   } else if (!fusion) {
     double l1 = INFINITY;
     gg_udf_state ust{acc.p, contrib.p, 0};

@@ -25,7 +25,7 @@
 //       dangling mass, next contrib) and acc reset; hub pass finishes split rows.
 // All per-vertex state lives in the renumbered id space; ranks are permuted
 // back on output.  Results equal the reference's up to f64 summation order.
-#include "prpull.cuh"
+#include "prtile.cuh"
 #include "apply.cuh"
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -35,12 +35,19 @@
 
 namespace gg {
 
+struct TileSeg {
+  const int64_t* tile_row;
+  const int64_t* tile_edge;
+  int64_t ntiles;
+};
+
 struct PrBlockLayout {
-  int64_t ns = 0, K = 0, V = 0, E = 0, hub_t = 0, nvrows = 0, nhubs = 0;
+  int64_t ns = 0, K = 0, V = 0, E = 0, nrows = 0;
   int ct_bytes = 0;
-  DevBuf<int32_t> newid, order, outdeg, src, vowner, hubs;
-  DevBuf<int64_t> voff;
-  std::vector<int64_t> seg_chunk;  // K+1 boundaries in 32-row chunks; segment 0 first
+  DevBuf<int32_t> newid, order, outdeg, src, owner;  // owner: cold pair -> destination
+  DevBuf<int64_t> roff;                              // all rows: hot [0,V) then cold pairs
+  std::vector<int64_t> seg_row;                      // K+1 row boundaries (segment 0 = hot)
+  std::vector<TilePlan> tiles;                       // per segment
   double prep_ms = 0;
 };
 
@@ -115,58 +122,44 @@ __global__ void k_pieces(const int64_t* start, int64_t n, int64_t end, int64_t h
     pieces[p] = q < 1 ? (min1 ? 1 : 0) : q;
   }
 }
-// hot rows: row v = destination v, edges [off0[v], off0[v+1])
-__global__ void k_fill_hot(const int64_t* off0, int64_t V, const int64_t* vstart, int64_t hub_t,
-                           int64_t* voff, int32_t* vowner, int32_t* hubs, unsigned long long* nh) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = off0[v], len = off0[v + 1] - lo, s = vstart[v];
-    if (len > hub_t) {
-      int64_t np = (len + hub_t - 1) / hub_t;
-      for (int64_t k = 0; k < np; ++k) {
-        voff[s + k] = lo + k * hub_t;
-        vowner[s + k] = ~(int32_t)v;
-      }
-      hubs[atomicAdd(nh, 1ULL)] = (int32_t)v;
-    } else {
-      voff[s] = lo;
-      vowner[s] = (int32_t)v;
-    }
-  }
-}
-// cold rows: pair p = (segment, dst) run starting at start[p]
-__global__ void k_fill_cold(const int64_t* start, const uint64_t* key, int64_t n, int64_t E,
-                            const int64_t* vstart, const int64_t* seg_first_vs,
-                            const int64_t* seg_base, int nvb, int64_t hub_t, int64_t* voff,
-                            int32_t* vowner) {
-  const uint64_t mask = (1ULL << nvb) - 1;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t lo = start[p];
-    const int64_t len = (p + 1 < n ? start[p + 1] : E) - lo;
-    const uint64_t k = key[lo] >> (32 + nvb);
-    const int32_t dst = (int32_t)((key[lo] >> 32) & mask);
-    const int64_t row = seg_base[k] + (vstart[p] - seg_first_vs[k]);
-    const int64_t np = (len + hub_t - 1) / hub_t;
-    for (int64_t q = 0; q < np; ++q) {
-      voff[row + q] = lo + q * hub_t;
-      vowner[row + q] = np > 1 ? ~dst : dst;
-    }
-  }
-}
-__global__ void k_fill_pad(int64_t* voff, int32_t* vowner, int64_t r0, int64_t r1, int64_t edge) {
-  for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    voff[r] = edge;
-    vowner[r] = INT32_MIN;
-  }
-}
-
 template <class T>
 static T dget(const T* p) {
   T h;
   GG_CUDA(cudaMemcpy(&h, p, sizeof(T), cudaMemcpyDeviceToHost));
   return h;
+}
+
+static void plan_tiles(const int64_t* roff, int64_t row0, int64_t nrows, int64_t nedges, int dev,
+                       TilePlan& tp, bool want_cross) {
+  tp.nrows = nrows;
+  tp.ntiles = (nrows + nedges + kTile - 1) / kTile;
+  tp.tile_row.alloc(tp.ntiles + 1);
+  tp.tile_edge.alloc(tp.ntiles + 1);
+  k_tile_starts<<<grid_for(tp.ntiles + 1, 256, dev), 256>>>(roff, nrows, row0, tp.ntiles, tp.tile_row.p,
+                                                              tp.tile_edge.p);
+  GG_LAUNCH_CHECK();
+  if (!want_cross) return;
+  DevBuf<uint8_t> mark(nrows + 1);
+  mark.zero();
+  if (tp.ntiles > 1)
+    k_mark_cross<<<grid_for(tp.ntiles, 256, dev), 256>>>(roff, tp.tile_row.p, tp.tile_edge.p, tp.ntiles,
+                                                         row0, nrows, mark.p);
+  GG_LAUNCH_CHECK();
+  tp.cross.alloc(nrows + 1);
+  DevBuf<unsigned long long> n(1);
+  cub::CountingInputIterator<int32_t> it((int32_t)0);
+  size_t temp = 0;
+  GG_CUDA(cub::DeviceSelect::Flagged(nullptr, temp, it, mark.p, tp.cross.p, n.p, nrows));
+  DevBuf<uint8_t> tb(temp);
+  GG_CUDA(cub::DeviceSelect::Flagged(tb.p, temp, it, mark.p, tp.cross.p, n.p, nrows));
+  tp.ncross = (int64_t)dget(n.p);
+}
+
+__global__ void k_pair_owner(const uint64_t* key, const int64_t* pstart, int64_t n, int nvb, int32_t* owner) {
+  const uint64_t mask = (1ULL << nvb) - 1;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    owner[p] = (int32_t)((key[pstart[p]] >> 32) & mask);
 }
 
 static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, int ct_bytes) {
@@ -181,7 +174,6 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   L->V = V;
   L->E = E;
   L->ct_bytes = ct_bytes;
-  L->hub_t = kPieceEdges;
   const int nvb = nbits((uint64_t)(V > 1 ? V - 1 : 1));
   const int kb = nbits((uint64_t)(L->K > 1 ? L->K - 1 : 1));
   if (32 + nvb + kb > 64) fail(GG_ERR_VALUE, "EdgeBlocking layout: too many segments for this graph");
@@ -217,111 +209,63 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   k_count_hot<<<grid_for(E, 256, dev), 256>>>(keys.p, E, shift, cnt.p);
   GG_LAUNCH_CHECK();
   const int64_t E0 = (int64_t)dget(cnt.p);
-  // 4a. sources + hot destination offsets
+  // 4. rows: [0, V) hot destinations (CSR over the hot edges), then the cold
+  //    (segment, destination) pairs; one offsets array for all rows.
   L->src.alloc(E);
-  DevBuf<int64_t> off0(V + 1);
-  {
-    DevBuf<int32_t> dh(E0 > 0 ? E0 : 1);
-    k_split_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->src.p, dh.p, E0);
-    GG_LAUNCH_CHECK();
-    offsets_from_sorted(dev, dh.p, E0, V, off0.p, 0);
-  }
-  // 4b. hot virtual rows
-  DevBuf<int64_t> hpieces(V), hvstart(V);
-  k_pieces<<<grid_for(V, 256, dev), 256>>>(off0.p, V, E0, L->hub_t, hpieces.p, 1);
-  // (k_pieces computes len from consecutive starts; off0 has V+1 entries so
-  // start[p+1] is off0[v+1] and `end` is unused for v < V)
-  size_t temp = 0;
-  GG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, hpieces.p, hvstart.p, V));
-  {
-    DevBuf<uint8_t> tb(temp);
-    GG_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, temp, hpieces.p, hvstart.p, V));
-  }
-  const int64_t hot_rows = dget(hvstart.p + V - 1) + dget(hpieces.p + V - 1);
-  const int64_t R0 = (hot_rows + 31) / 32 * 32;
-  // 4c. cold pairs
   const int64_t Ec = E - E0;
-  DevBuf<int64_t> pstart(Ec > 0 ? Ec : 1);
+  DevBuf<int64_t> pstart(Ec + 1);
   DevBuf<unsigned long long> npairs(1);
   npairs.zero();
   int64_t P = 0;
   if (Ec > 0) {
     cub::CountingInputIterator<int64_t> it(E0);
     RunStart pred{keys.p, E0};
-    temp = 0;
+    size_t temp = 0;
     GG_CUDA(cub::DeviceSelect::If(nullptr, temp, it, pstart.p, npairs.p, Ec, pred));
     DevBuf<uint8_t> tb(temp);
     GG_CUDA(cub::DeviceSelect::If(tb.p, temp, it, pstart.p, npairs.p, Ec, pred));
     P = (int64_t)dget(npairs.p);
   }
-  DevBuf<int64_t> cpieces(P > 0 ? P : 1), cvstart(P > 0 ? P : 1);
-  std::vector<int64_t> seg_first_pair(L->K + 1, P), seg_rows(L->K, 0);
-  std::vector<int64_t> seg_base(L->K + 1, 0), seg_first_vs(L->K, 0), seg_end_edge(L->K, E);
-  if (P > 0) {
-    k_pieces<<<grid_for(P, 256, dev), 256>>>(pstart.p, P, E, L->hub_t, cpieces.p, 1);
-    temp = 0;
-    GG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, cpieces.p, cvstart.p, P));
-    DevBuf<uint8_t> tb(temp);
-    GG_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, temp, cpieces.p, cvstart.p, P));
-    // segment of every pair start (host: K is small) -> first pair per segment
-    std::vector<int64_t> hstart(P);
-    GG_CUDA(cudaMemcpy(hstart.data(), pstart.p, P * 8, cudaMemcpyDeviceToHost));
-    std::vector<int64_t> hvs(P), hpc(P);
-    GG_CUDA(cudaMemcpy(hvs.data(), cvstart.p, P * 8, cudaMemcpyDeviceToHost));
-    GG_CUDA(cudaMemcpy(hpc.data(), cpieces.p, P * 8, cudaMemcpyDeviceToHost));
-    // binary search the segment boundaries through the sorted keys
-    auto seg_of_edge = [&](int64_t e) { return (int64_t)(dget(keys.p + e) >> shift); };
-    for (int64_t k = 1; k < L->K; ++k) {
-      int64_t lo = 0, hi = P;  // first pair with segment >= k
-      while (lo < hi) {
-        int64_t mid = (lo + hi) / 2;
-        if (seg_of_edge(hstart[mid]) < k) lo = mid + 1; else hi = mid;
-      }
-      seg_first_pair[k] = lo;
-    }
-    seg_first_pair[0] = 0;
-    for (int64_t k = 1; k < L->K; ++k) {
-      const int64_t a = seg_first_pair[k];
-      const int64_t bb = (k + 1 < L->K) ? seg_first_pair[k + 1] : P;
-      seg_first_vs[k] = a < P ? hvs[a] : (P ? hvs[P - 1] + hpc[P - 1] : 0);
-      const int64_t end_vs = bb < P ? hvs[bb] : (hvs[P - 1] + hpc[P - 1]);
-      seg_rows[k] = end_vs - seg_first_vs[k];
-      seg_end_edge[k] = bb < P ? hstart[bb] : E;
-    }
-  }
-  // row layout: [hot R0][seg1 padded]...[segK-1 padded]
-  seg_base[0] = 0;
-  seg_base[1] = R0;
-  for (int64_t k = 1; k < L->K; ++k) seg_base[k + 1] = seg_base[k] + (seg_rows[k] + 31) / 32 * 32;
-  L->nvrows = seg_base[L->K];
-  L->voff.alloc(L->nvrows + 1);
-  L->vowner.alloc(L->nvrows + 1);
-  L->hubs.alloc(V);
-  DevBuf<unsigned long long> nh(1);
-  nh.zero();
-  k_fill_hot<<<grid_for(V, 256, dev), 256>>>(off0.p, V, hvstart.p, L->hub_t, L->voff.p, L->vowner.p,
-                                             L->hubs.p, nh.p);
-  k_fill_pad<<<grid_for(R0 - hot_rows + 1, 256, dev), 256>>>(L->voff.p, L->vowner.p, hot_rows, R0, E0);
-  GG_LAUNCH_CHECK();
-  if (P > 0) {
-    DevBuf<int64_t> d_sfv(L->K), d_base(L->K + 1);
-    GG_CUDA(cudaMemcpy(d_sfv.p, seg_first_vs.data(), L->K * 8, cudaMemcpyHostToDevice));
-    GG_CUDA(cudaMemcpy(d_base.p, seg_base.data(), (L->K + 1) * 8, cudaMemcpyHostToDevice));
-    k_fill_cold<<<grid_for(P, 256, dev), 256>>>(pstart.p, keys.p, P, E, cvstart.p, d_sfv.p, d_base.p, nvb,
-                                                L->hub_t, L->voff.p, L->vowner.p);
+  L->nrows = V + P;
+  L->roff.alloc(V + P + 1);
+  {
+    DevBuf<int32_t> dh(E0 > 0 ? E0 : 1);
+    k_split_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->src.p, dh.p, E0);
     GG_LAUNCH_CHECK();
-    for (int64_t k = 1; k < L->K; ++k) {
-      const int64_t r0 = seg_base[k] + seg_rows[k], r1 = seg_base[k + 1];
-      if (r1 > r0)
-        k_fill_pad<<<grid_for(r1 - r0, 256, dev), 256>>>(L->voff.p, L->vowner.p, r0, r1, seg_end_edge[k]);
-    }
+    offsets_from_sorted(dev, dh.p, E0, V, L->roff.p, 0);  // roff[0..V], roff[V] = E0
+  }
+  if (P > 0) {
+    GG_CUDA(cudaMemcpy(L->roff.p + V, pstart.p, P * 8, cudaMemcpyDeviceToDevice));
+    L->owner.alloc(P);
+    k_pair_owner<<<grid_for(P, 256, dev), 256>>>(keys.p, pstart.p, P, nvb, L->owner.p);
     GG_LAUNCH_CHECK();
   }
-  k_fill_pad<<<1, 32>>>(L->voff.p, L->vowner.p, L->nvrows, L->nvrows + 1, E);
-  GG_LAUNCH_CHECK();
-  L->nhubs = (int64_t)dget(nh.p);
-  L->seg_chunk.resize(L->K + 1);
-  for (int64_t k = 0; k <= L->K; ++k) L->seg_chunk[k] = seg_base[k] / 32;
+  GG_CUDA(cudaMemcpy(L->roff.p + V + P, &E, 8, cudaMemcpyHostToDevice));
+  // segment row ranges: cold pairs are sorted by segment; find boundaries by
+  // binary search through the pair keys (K is small)
+  L->seg_row.assign(L->K + 1, V + P);
+  L->seg_row[0] = 0;
+  if (L->K > 1) L->seg_row[1] = V;
+  for (int64_t k = 2; k < L->K; ++k) {
+    int64_t lo = 0, hi = P;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      int64_t e = dget(pstart.p + mid);
+      if ((int64_t)(dget(keys.p + e) >> shift) < k) lo = mid + 1; else hi = mid;
+    }
+    L->seg_row[k] = V + lo;
+  }
+  // 5. merge-path tiles per segment (+ crossing rows of the hot segment)
+  L->tiles.resize(L->K);
+  for (int64_t k = 0; k < L->K; ++k) {
+    const int64_t r0 = L->seg_row[k], r1 = L->seg_row[k + 1];
+    const int64_t e_lo = k == 0 ? 0 : (r1 > r0 ? -1 : 0);
+    (void)e_lo;
+    int64_t ea = 0, eb = 0;
+    GG_CUDA(cudaMemcpy(&ea, L->roff.p + r0, 8, cudaMemcpyDeviceToHost));
+    GG_CUDA(cudaMemcpy(&eb, L->roff.p + r1, 8, cudaMemcpyDeviceToHost));
+    plan_tiles(L->roff.p, r0, r1 - r0, eb - ea, dev, L->tiles[k], k == 0);
+  }
   GG_CUDA(cudaDeviceSynchronize());
   L->prep_ms = now_ms() - t0;
   return L;
@@ -373,26 +317,36 @@ __global__ void k_unpermute(const double* rank_new, const int32_t* newid, int64_
     out[v] = rank_new[newid[v]];
 }
 
+// Whole loop in one cooperative launch (kernel fusion on "s0").
 template <class CT>
-static __global__ void __launch_bounds__(256) k_prb_fused(PrPullArgs<CT> a, CT* c0, CT* c1,
-                                                          const int64_t* seg_chunk, int64_t K,
-                                                          int64_t max_iters, double tol,
-                                                          int64_t* iters_out) {
-  __shared__ double s_acc[8 * 32];
+static __global__ void __launch_bounds__(kTileThreads) k_prb_fused(TileArgs<CT> a, CT* c0, CT* c1,
+                                                                   const TileSeg* segs, int64_t K,
+                                                                   const int32_t* cross, int64_t ncross,
+                                                                   int64_t max_iters, double tol,
+                                                                   int64_t* iters_out) {
+  __shared__ double s_val[kTile];
+  __shared__ int32_t s_rend[kTile + 1];
+  __shared__ double s_rowsum[kTile + 1];
   cg::grid_group grid = cg::this_grid();
   a.coherent = 1;
+  const int32_t* cold_owner = a.owner;
   int64_t it = 0;
   double l1 = INFINITY;
   while (!(it >= max_iters || l1 < tol)) {
     a.contrib = (it & 1) ? c1 : c0;
     a.contrib_next = (it & 1) ? c0 : c1;
-    for (int64_t k = 1; k < K; ++k) {
-      pr_pull_chunks<CT, 1>(a, it, s_acc, seg_chunk[k], seg_chunk[k + 1]);
+    for (int64_t k = 1; k <= K; ++k) {  // cold segments first, hot (k == K -> 0) last
+      const TileSeg& sg = segs[k == K ? 0 : k];
+      a.owner = k == K ? nullptr : cold_owner;  // hot rows are destinations, cold rows pairs
+      a.row_base = k == K ? 0 : a.V;
+      a.tile_row = sg.tile_row;
+      a.tile_edge = sg.tile_edge;
+      a.ntiles = sg.ntiles;
+      if (k == K) pr_tiles<CT, 2>(a, it, s_val, s_rend, s_rowsum);
+      else pr_tiles<CT, 1>(a, it, s_val, s_rend, s_rowsum);
       grid.sync();
     }
-    pr_pull_chunks<CT, 2>(a, it, s_acc, seg_chunk[0], seg_chunk[1]);
-    grid.sync();
-    pr_pull_hubs(a, it);
+    pr_crossing(a, it, cross, ncross);
     grid.sync();
     l1 = *((volatile double*)a.scal + 2 * it + 1);
     ++it;
@@ -415,27 +369,48 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank.p, c0.p, scal.p);
   GG_LAUNCH_CHECK();
   count_launch();
-  PrPullArgs<CT> a{L->voff.p, L->vowner.p, L->nvrows / 32, L->src.p, c0.p, c1.p, rank.p,
-                   L->outdeg.p, acc.p, L->hubs.p, L->nhubs, scal.p, V, damping};
+  TileArgs<CT> a{};
+  a.roff = L->roff.p;
+  a.owner = L->owner.p;  // cold rows only (row_base = V); hot rows are identity
+  a.row_base = V;
+  a.src = L->src.p;
+  a.rank = rank.p;
+  a.outdeg = L->outdeg.p;
+  a.acc = acc.p;
+  a.hubsum = acc.p;
+  a.scal = scal.p;
+  a.V = V;
+  a.damping = damping;
+  const TilePlan& hot = L->tiles[0];
   int64_t it = 0;
   if (!fusion) {
     double l1 = INFINITY;
-    const unsigned grid = (unsigned)sm_count(dev) * 8;
-    const unsigned hgrid = grid_for(L->nhubs, 256, dev);
+    const unsigned grid = (unsigned)sm_count(dev) * 5;
+    const unsigned cgrid = grid_for(hot.ncross, 256, dev);
     while (!(it >= max_iters || l1 < tol)) {
       a.contrib = (it & 1) ? c1.p : c0.p;
       a.contrib_next = (it & 1) ? c0.p : c1.p;
       rt.edge_begin();
       for (int64_t k = 1; k < L->K; ++k) {
-        if (L->seg_chunk[k + 1] > L->seg_chunk[k]) {
-          k_pr_seg<CT, 1><<<grid, 256, 0, st>>>(a, it, L->seg_chunk[k], L->seg_chunk[k + 1]);
-          count_launch();
-        }
+        const TilePlan& tp = L->tiles[k];
+        if (!tp.ntiles) continue;
+        a.tile_row = tp.tile_row.p;
+        a.tile_edge = tp.tile_edge.p;
+        a.ntiles = tp.ntiles;
+        a.owner = L->owner.p;
+        a.row_base = V;
+        k_pr_tiles<CT, 1><<<grid, kTileThreads, 0, st>>>(a, it);
+        count_launch();
       }
-      k_pr_seg<CT, 2><<<grid, 256, 0, st>>>(a, it, L->seg_chunk[0], L->seg_chunk[1]);
+      a.tile_row = hot.tile_row.p;
+      a.tile_edge = hot.tile_edge.p;
+      a.ntiles = hot.ntiles;
+      a.owner = nullptr;
+      a.row_base = 0;
+      k_pr_tiles<CT, 2><<<grid, kTileThreads, 0, st>>>(a, it);
       count_launch();
-      if (L->nhubs) {
-        k_pr_pull_hubs<CT><<<hgrid, 256, 0, st>>>(a, it);
+      if (hot.ncross) {
+        k_pr_crossing<CT><<<cgrid, 256, 0, st>>>(a, it, hot.cross.p, hot.ncross);
         count_launch();
       }
       rt.edge_end();
@@ -449,17 +424,23 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
       }
     }
   } else {
-    DevBuf<int64_t> iters(1), segc(L->K + 1);
-    GG_CUDA(cudaMemcpyAsync(segc.p, L->seg_chunk.data(), (L->K + 1) * 8, cudaMemcpyHostToDevice, st));
-    int blocks = max_coop_blocks((const void*)k_prb_fused<CT>, 256, dev);
+    std::vector<TileSeg> hs(L->K);
+    for (int64_t k = 0; k < L->K; ++k)
+      hs[k] = TileSeg{L->tiles[k].tile_row.p, L->tiles[k].tile_edge.p, L->tiles[k].ntiles};
+    DevBuf<TileSeg> segs(L->K);
+    GG_CUDA(cudaMemcpyAsync(segs.p, hs.data(), L->K * sizeof(TileSeg), cudaMemcpyHostToDevice, st));
+    DevBuf<int64_t> iters(1);
+    int blocks = max_coop_blocks((const void*)k_prb_fused<CT>, kTileThreads, dev);
     CT* p0 = c0.p;
     CT* p1 = c1.p;
-    const int64_t* sc = segc.p;
+    const TileSeg* sp = segs.p;
     int64_t K = L->K;
+    const int32_t* cr = hot.cross.p;
+    int64_t nc = hot.ncross;
     int64_t* ip = iters.p;
-    void* args[] = {&a, &p0, &p1, &sc, &K, &max_iters, &tol, &ip};
+    void* args[] = {&a, &p0, &p1, &sp, &K, &cr, &nc, &max_iters, &tol, &ip};
     rt.edge_begin();
-    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_prb_fused<CT>, blocks, 256, args, 0, st));
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_prb_fused<CT>, blocks, kTileThreads, args, 0, st));
     rt.edge_end();
     count_launch();
     it = dget(iters.p);
