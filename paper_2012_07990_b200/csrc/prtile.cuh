@@ -85,11 +85,21 @@ __device__ __forceinline__ void pr_tiles(const TileArgs<CT>& a, int64_t it, doub
     int i = lo, j = d0 - lo;
     double sum = 0.0;
     const int total_items = nr + ne;
+    // rows started and ended inside this thread's items are stored directly;
+    // the first row's partial (head) and the open last row (tail) are
+    // combined across threads by a segmented scan -- no shared atomics.
+    int head_row = -1;
+    double head_val = 0.0;
 #pragma unroll
     for (int q = 0; q < kIpt; ++q) {
       if (d0 + q < total_items) {
         if (i < nr && j == s_rend[i]) {
-          if (sum != 0.0) smem_add(s_rowsum + i, sum);
+          if (head_row < 0) {
+            head_row = i;
+            head_val = sum;
+          } else {
+            s_rowsum[i] = sum;
+          }
           sum = 0.0;
           ++i;
         } else {
@@ -98,14 +108,59 @@ __device__ __forceinline__ void pr_tiles(const TileArgs<CT>& a, int64_t it, doub
         }
       }
     }
-    if (sum != 0.0) {
-      if (i < nr) {
-        smem_add(s_rowsum + i, sum);
-      } else {  // row `re` continues into the next tile: crossing row
-        const int64_t r = re;
-        const int32_t o = a.owner ? a.owner[r - a.row_base] : (int32_t)(r - a.row_base);
-        atomicAdd(a.hubsum + o, sum);
+    // segmented inclusive scan of the tails (rows are nondecreasing in tid)
+    int trow = i;
+    double tval = sum;
+    const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      double v = __shfl_up_sync(0xffffffffu, tval, o);
+      int r = __shfl_up_sync(0xffffffffu, trow, o);
+      if (lane >= o && r == trow) tval += v;
+    }
+    __shared__ int s_wrow_first[kTileThreads / 32], s_wrow_last[kTileThreads / 32];
+    __shared__ double s_wval[kTileThreads / 32];
+    __shared__ int s_win_row[kTileThreads / 32];
+    __shared__ double s_win_val[kTileThreads / 32];
+    if (lane == 0) s_wrow_first[w] = trow;
+    if (lane == 31) {
+      s_wrow_last[w] = trow;
+      s_wval[w] = tval;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int crow = -2;
+      double cval = 0.0;
+      for (int k = 0; k < kTileThreads / 32; ++k) {
+        s_win_row[k] = crow;
+        s_win_val[k] = cval;
+        if (s_wrow_first[k] == s_wrow_last[k] && s_wrow_last[k] == crow) {
+          cval += s_wval[k];
+        } else {
+          crow = s_wrow_last[k];
+          cval = s_wval[k];
+        }
       }
+    }
+    __syncthreads();
+    if (trow == s_win_row[w]) tval += s_win_val[w];
+    // publish each thread's scanned tail for its successor; the tile's last
+    // open row (row `re`, continuing into the next tile) is a crossing row
+    double* s_tval = s_val;  // edge values are no longer needed
+    int32_t* s_trow = reinterpret_cast<int32_t*>(s_val + kTileThreads);
+    __syncthreads();
+    s_tval[tid] = tval;
+    s_trow[tid] = trow;
+    __syncthreads();
+    if (head_row >= 0) {
+      double tot = head_val;
+      if (tid > 0 && s_trow[tid - 1] == head_row) tot += s_tval[tid - 1];
+      s_rowsum[head_row] = tot;
+    }
+    if (tid == kTileThreads - 1 && trow >= nr && tval != 0.0) {
+      const int64_t r = re;
+      const int32_t o = a.owner ? a.owner[r - a.row_base] : (int32_t)(r - a.row_base);
+      atomicAdd(a.hubsum + o, tval);
     }
     __syncthreads();
     // 4. finish the rows whose END is in this tile
