@@ -45,6 +45,8 @@ struct PrBlockLayout {
   int64_t ns = 0, K = 0, V = 0, E = 0, nrows = 0;
   int ct_bytes = 0;
   DevBuf<int32_t> newid, order, outdeg, src, owner;  // owner: cold pair -> destination
+  DevBuf<int32_t> dst;                               // destination of every blocked edge
+  std::vector<int64_t> seg_edge;                     // K+1 edge boundaries (segment 0 = hot)
   DevBuf<int64_t> roff;                              // all rows: hot [0,V) then cold pairs
   std::vector<int64_t> seg_row;                      // K+1 row boundaries (segment 0 = hot)
   std::vector<TilePlan> tiles;                       // per segment
@@ -97,6 +99,12 @@ struct IsCold {
   int shift;
   __device__ __forceinline__ bool operator()(int64_t e) const { return (key[e] >> shift) != 0; }
 };
+__global__ void k_dst_of_keys(const uint64_t* key, int64_t E, int nvb, int32_t* dst) {
+  const uint64_t mask = (1ULL << nvb) - 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = (int32_t)((key[e] >> 32) & mask);
+}
 __global__ void k_count_hot(const uint64_t* key, int64_t E, int shift, unsigned long long* n) {
   unsigned long long c = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
@@ -183,6 +191,7 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
     DevBuf<int32_t> ids(V);
     L->order.alloc(V);
     k_neg_deg<<<grid_for(V, 256, dev), 256>>>(out.off, V, key.p, ids.p);
+    if (getenv("GG_PR_NO_RELABEL")) GG_CUDA(cudaMemset(key.p, 0, V * sizeof(uint32_t)));  // ablation
     size_t temp = 0;
     GG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, key.p, key2.p, ids.p, L->order.p, V));
     DevBuf<uint8_t> tb(temp);
@@ -212,6 +221,9 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   // 4. rows: [0, V) hot destinations (CSR over the hot edges), then the cold
   //    (segment, destination) pairs; one offsets array for all rows.
   L->src.alloc(E);
+  L->dst.alloc(E);
+  k_dst_of_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->dst.p);
+  GG_LAUNCH_CHECK();
   const int64_t Ec = E - E0;
   DevBuf<int64_t> pstart(Ec + 1);
   DevBuf<unsigned long long> npairs(1);
@@ -255,6 +267,8 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
     }
     L->seg_row[k] = V + lo;
   }
+  L->seg_edge.resize(L->K + 1);
+  for (int64_t k = 0; k <= L->K; ++k) L->seg_edge[k] = dget(L->roff.p + L->seg_row[k]);
   // 5. merge-path tiles per segment (+ crossing rows of the hot segment)
   L->tiles.resize(L->K);
   for (int64_t k = 0; k < L->K; ++k) {
@@ -317,38 +331,108 @@ __global__ void k_unpermute(const double* rank_new, const int32_t* newid, int64_
     out[v] = rank_new[newid[v]];
 }
 
+// ---------------------------------------------------------------------------
+// Edge phase (EDGE_ONLY semantics, Alg. 2): for one segment, every warp takes
+// kU*32 consecutive blocked edges per step -- coalesced (src, dst) loads, kU
+// independent gathers per lane, then a warp segmented scan keyed by the
+// (sorted) destination so each destination run issues ONE f64 add to acc.
+// ---------------------------------------------------------------------------
+template <class CT>
+__device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                             int64_t e0, int64_t e1, const CT* contrib, double* acc,
+                                             int coherent) {
+  constexpr int kU = 8;
+  const int lane = lane_id();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = e0 + warp * 32 * kU; base < e1; base += nwarps * 32 * kU) {
+    int32_t su[kU], dv[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int64_t e = base + q * 32 + lane;
+      const bool live = e < e1;
+      su[q] = live ? __ldcs(src + e) : 0;
+      dv[q] = live ? __ldcs(dst + e) : -1;
+    }
+    double v[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q)
+      v[q] = dv[q] >= 0 ? (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q])) : 0.0;
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int d = dv[q];
+      double x = v[q];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        double t = __shfl_up_sync(0xffffffffu, x, o);
+        int dd = __shfl_up_sync(0xffffffffu, d, o);
+        if (lane >= o && dd == d) x += t;
+      }
+      const int dn = __shfl_down_sync(0xffffffffu, d, 1);
+      if (d >= 0 && (lane == 31 || dn != d)) atomicAdd(acc + d, x);
+    }
+  }
+}
+
+template <class CT>
+static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, const int32_t* dst, int64_t e0,
+                                                         int64_t e1, const CT* contrib, double* acc) {
+  pr_edges_seg<CT>(src, dst, e0, e1, contrib, acc, 0);
+}
+
+// vertex pass: rank' = base + d*acc, L1, next dangling mass, next contrib, acc reset
+template <class CT>
+__device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* outdeg, double* rank, CT* contrib_next,
+                                               double* acc, double* scal, int64_t it, double damping) {
+  const double n = (double)V;
+  const double base = (1.0 - damping) / n + damping * scal[2 * it] / n;
+  double l1 = 0, dm = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double nv = base + damping * acc[v];
+    acc[v] = 0.0;
+    l1 += fabs(nv - rank[v]);
+    rank[v] = nv;
+    const int32_t od = __ldg(outdeg + v);
+    if (od) contrib_next[v] = (CT)(nv / (double)od);
+    else dm += nv;
+  }
+  l1 = block_sum(l1);
+  dm = block_sum(dm);
+  if (threadIdx.x == 0) {
+    if (l1 != 0.0) atomicAdd(scal + 2 * it + 1, l1);
+    if (dm != 0.0) atomicAdd(scal + 2 * (it + 1), dm);
+  }
+}
+
+template <class CT>
+static __global__ void __launch_bounds__(256) k_pr_vertex(int64_t V, const int32_t* outdeg, double* rank,
+                                                          CT* contrib_next, double* acc, double* scal,
+                                                          int64_t it, double damping) {
+  pr_vertex_pass<CT>(V, outdeg, rank, contrib_next, acc, scal, it, damping);
+}
+
 // Whole loop in one cooperative launch (kernel fusion on "s0").
 template <class CT>
-static __global__ void __launch_bounds__(kTileThreads) k_prb_fused(TileArgs<CT> a, CT* c0, CT* c1,
-                                                                   const TileSeg* segs, int64_t K,
-                                                                   const int32_t* cross, int64_t ncross,
-                                                                   int64_t max_iters, double tol,
-                                                                   int64_t* iters_out) {
-  __shared__ double s_val[kTile];
-  __shared__ int32_t s_rend[kTile + 1];
-  __shared__ double s_rowsum[kTile + 1];
+static __global__ void __launch_bounds__(256) k_prb_fused(const int32_t* src, const int32_t* dst,
+                                                          const int64_t* seg_edge, int64_t K, int64_t V,
+                                                          const int32_t* outdeg, double* rank, CT* c0, CT* c1,
+                                                          double* acc, double* scal, int64_t max_iters,
+                                                          double tol, double damping, int64_t* iters_out) {
   cg::grid_group grid = cg::this_grid();
-  a.coherent = 1;
-  const int32_t* cold_owner = a.owner;
   int64_t it = 0;
   double l1 = INFINITY;
   while (!(it >= max_iters || l1 < tol)) {
-    a.contrib = (it & 1) ? c1 : c0;
-    a.contrib_next = (it & 1) ? c0 : c1;
-    for (int64_t k = 1; k <= K; ++k) {  // cold segments first, hot (k == K -> 0) last
-      const TileSeg& sg = segs[k == K ? 0 : k];
-      a.owner = k == K ? nullptr : cold_owner;  // hot rows are destinations, cold rows pairs
-      a.row_base = k == K ? 0 : a.V;
-      a.tile_row = sg.tile_row;
-      a.tile_edge = sg.tile_edge;
-      a.ntiles = sg.ntiles;
-      if (k == K) pr_tiles<CT, 2>(a, it, s_val, s_rend, s_rowsum);
-      else pr_tiles<CT, 1>(a, it, s_val, s_rend, s_rowsum);
+    const CT* cur = (it & 1) ? c1 : c0;
+    CT* nxt = (it & 1) ? c0 : c1;
+    for (int64_t k = 1; k <= K; ++k) {  // cold segments, then the hot one
+      const int64_t s = k == K ? 0 : k;
+      pr_edges_seg<CT>(src, dst, seg_edge[s], seg_edge[s + 1], cur, acc, 1);
       grid.sync();
     }
-    pr_crossing(a, it, cross, ncross);
+    pr_vertex_pass<CT>(V, outdeg, rank, nxt, acc, scal, it, damping);
     grid.sync();
-    l1 = *((volatile double*)a.scal + 2 * it + 1);
+    l1 = *((volatile double*)scal + 2 * it + 1);
     ++it;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *iters_out = it;
@@ -369,51 +453,25 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank.p, c0.p, scal.p);
   GG_LAUNCH_CHECK();
   count_launch();
-  TileArgs<CT> a{};
-  a.roff = L->roff.p;
-  a.owner = L->owner.p;  // cold rows only (row_base = V); hot rows are identity
-  a.row_base = V;
-  a.src = L->src.p;
-  a.rank = rank.p;
-  a.outdeg = L->outdeg.p;
-  a.acc = acc.p;
-  a.hubsum = acc.p;
-  a.scal = scal.p;
-  a.V = V;
-  a.damping = damping;
-  const TilePlan& hot = L->tiles[0];
   int64_t it = 0;
   if (!fusion) {
     double l1 = INFINITY;
-    const unsigned grid = (unsigned)sm_count(dev) * 5;
-    const unsigned cgrid = grid_for(hot.ncross, 256, dev);
+    const unsigned grid = (unsigned)sm_count(dev) * 8;
     while (!(it >= max_iters || l1 < tol)) {
-      a.contrib = (it & 1) ? c1.p : c0.p;
-      a.contrib_next = (it & 1) ? c0.p : c1.p;
+      const CT* cur = (it & 1) ? c1.p : c0.p;
+      CT* nxt = (it & 1) ? c0.p : c1.p;
       rt.edge_begin();
-      for (int64_t k = 1; k < L->K; ++k) {
-        const TilePlan& tp = L->tiles[k];
-        if (!tp.ntiles) continue;
-        a.tile_row = tp.tile_row.p;
-        a.tile_edge = tp.tile_edge.p;
-        a.ntiles = tp.ntiles;
-        a.owner = L->owner.p;
-        a.row_base = V;
-        k_pr_tiles<CT, 1><<<grid, kTileThreads, 0, st>>>(a, it);
-        count_launch();
-      }
-      a.tile_row = hot.tile_row.p;
-      a.tile_edge = hot.tile_edge.p;
-      a.ntiles = hot.ntiles;
-      a.owner = nullptr;
-      a.row_base = 0;
-      k_pr_tiles<CT, 2><<<grid, kTileThreads, 0, st>>>(a, it);
-      count_launch();
-      if (hot.ncross) {
-        k_pr_crossing<CT><<<cgrid, 256, 0, st>>>(a, it, hot.cross.p, hot.ncross);
+      for (int64_t k = 1; k <= L->K; ++k) {  // Alg. 2: segments in order, cold first, hot last
+        const int64_t sg = k == L->K ? 0 : k;
+        const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
+        if (e1 <= e0) continue;
+        k_pr_edges<CT><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
         count_launch();
       }
       rt.edge_end();
+      k_pr_vertex<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(V, L->outdeg.p, rank.p, nxt, acc.p, scal.p, it,
+                                                             damping);
+      count_launch();
       GG_LAUNCH_CHECK();
       rt.stats.dispatch_count += 1;
       rt.stats.direction_log.push_back(s.direction);
@@ -424,23 +482,24 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
       }
     }
   } else {
-    std::vector<TileSeg> hs(L->K);
-    for (int64_t k = 0; k < L->K; ++k)
-      hs[k] = TileSeg{L->tiles[k].tile_row.p, L->tiles[k].tile_edge.p, L->tiles[k].ntiles};
-    DevBuf<TileSeg> segs(L->K);
-    GG_CUDA(cudaMemcpyAsync(segs.p, hs.data(), L->K * sizeof(TileSeg), cudaMemcpyHostToDevice, st));
-    DevBuf<int64_t> iters(1);
-    int blocks = max_coop_blocks((const void*)k_prb_fused<CT>, kTileThreads, dev);
+    DevBuf<int64_t> iters(1), segs(L->K + 1);
+    GG_CUDA(cudaMemcpyAsync(segs.p, L->seg_edge.data(), (L->K + 1) * 8, cudaMemcpyHostToDevice, st));
+    int blocks = max_coop_blocks((const void*)k_prb_fused<CT>, 256, dev);
+    const int32_t* sp = L->src.p;
+    const int32_t* dp = L->dst.p;
+    const int64_t* se = segs.p;
+    int64_t K = L->K;
+    int64_t Vv = V;
+    const int32_t* od = L->outdeg.p;
+    double* rk = rank.p;
     CT* p0 = c0.p;
     CT* p1 = c1.p;
-    const TileSeg* sp = segs.p;
-    int64_t K = L->K;
-    const int32_t* cr = hot.cross.p;
-    int64_t nc = hot.ncross;
+    double* ac = acc.p;
+    double* sc = scal.p;
     int64_t* ip = iters.p;
-    void* args[] = {&a, &p0, &p1, &sp, &K, &cr, &nc, &max_iters, &tol, &ip};
+    void* args[] = {&sp, &dp, &se, &K, &Vv, &od, &rk, &p0, &p1, &ac, &sc, &max_iters, &tol, &damping, &ip};
     rt.edge_begin();
-    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_prb_fused<CT>, blocks, kTileThreads, args, 0, st));
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_prb_fused<CT>, blocks, 256, args, 0, st));
     rt.edge_end();
     count_launch();
     it = dget(iters.p);
