@@ -51,6 +51,11 @@ struct PrBlockLayout {
   std::vector<int64_t> seg_row;                      // K+1 row boundaries (segment 0 = hot)
   std::vector<TilePlan> tiles;                       // per segment
   double prep_ms = 0;
+  // per-run work buffers, kept across calls (cudaMalloc/cudaFree of GB-sized
+  // buffers per call would dominate short runs)
+  DevBuf<double> w_rank, w_acc, w_scal, w_out;
+  DevBuf<uint8_t> w_c0, w_c1;
+  std::mutex w_mu;
 };
 
 static int nbits(uint64_t x) {
@@ -269,17 +274,6 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   }
   L->seg_edge.resize(L->K + 1);
   for (int64_t k = 0; k <= L->K; ++k) L->seg_edge[k] = dget(L->roff.p + L->seg_row[k]);
-  // 5. merge-path tiles per segment (+ crossing rows of the hot segment)
-  L->tiles.resize(L->K);
-  for (int64_t k = 0; k < L->K; ++k) {
-    const int64_t r0 = L->seg_row[k], r1 = L->seg_row[k + 1];
-    const int64_t e_lo = k == 0 ? 0 : (r1 > r0 ? -1 : 0);
-    (void)e_lo;
-    int64_t ea = 0, eb = 0;
-    GG_CUDA(cudaMemcpy(&ea, L->roff.p + r0, 8, cudaMemcpyDeviceToHost));
-    GG_CUDA(cudaMemcpy(&eb, L->roff.p + r1, 8, cudaMemcpyDeviceToHost));
-    plan_tiles(L->roff.p, r0, r1 - r0, eb - ea, dev, L->tiles[k], k == 0);
-  }
   GG_CUDA(cudaDeviceSynchronize());
   L->prep_ms = now_ms() - t0;
   return L;
@@ -341,36 +335,78 @@ template <class CT>
 __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                              int64_t e0, int64_t e1, const CT* contrib, double* acc,
                                              int coherent) {
-  constexpr int kU = 8;
+  // Each lane owns 8 consecutive edges (two 16-byte loads per array), so a
+  // warp step covers 256 edges.  Runs of equal destination inside a lane are
+  // summed in registers; runs crossing lanes are joined by ONE warp segmented
+  // scan per step (instead of one per 32 edges).
+  constexpr int kE = 8;
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t base = e0 + warp * 32 * kU; base < e1; base += nwarps * 32 * kU) {
-    int32_t su[kU], dv[kU];
+  const int64_t start = e0 & ~int64_t(kE - 1);  // 32-byte aligned start
+  for (int64_t base = start + warp * 32 * kE; base < e1; base += nwarps * 32 * kE) {
+    const int64_t my = base + lane * kE;
+    int32_t su[kE], dv[kE];
+    if (my + kE <= e1 && my >= e0) {
+      const int4* s4 = reinterpret_cast<const int4*>(src + my);
+      const int4* d4 = reinterpret_cast<const int4*>(dst + my);
+      int4 a0 = __ldcs(s4), a1 = __ldcs(s4 + 1), b0 = __ldcs(d4), b1 = __ldcs(d4 + 1);
+      su[0] = a0.x; su[1] = a0.y; su[2] = a0.z; su[3] = a0.w;
+      su[4] = a1.x; su[5] = a1.y; su[6] = a1.z; su[7] = a1.w;
+      dv[0] = b0.x; dv[1] = b0.y; dv[2] = b0.z; dv[3] = b0.w;
+      dv[4] = b1.x; dv[5] = b1.y; dv[6] = b1.z; dv[7] = b1.w;
+    } else {
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int64_t e = base + q * 32 + lane;
-      const bool live = e < e1;
-      su[q] = live ? __ldcs(src + e) : 0;
-      dv[q] = live ? __ldcs(dst + e) : -1;
-    }
-    double v[kU];
-#pragma unroll
-    for (int q = 0; q < kU; ++q)
-      v[q] = dv[q] >= 0 ? (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q])) : 0.0;
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int d = dv[q];
-      double x = v[q];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        double t = __shfl_up_sync(0xffffffffu, x, o);
-        int dd = __shfl_up_sync(0xffffffffu, d, o);
-        if (lane >= o && dd == d) x += t;
+      for (int q = 0; q < kE; ++q) {
+        const int64_t e = my + q;
+        const bool live = e >= e0 && e < e1;
+        su[q] = live ? __ldcs(src + e) : 0;
+        dv[q] = live ? __ldcs(dst + e) : -1;
       }
-      const int dn = __shfl_down_sync(0xffffffffu, d, 1);
-      if (d >= 0 && (lane == 31 || dn != d)) atomicAdd(acc + d, x);
     }
+    double v[kE];
+#pragma unroll
+    for (int q = 0; q < kE; ++q)
+      v[q] = dv[q] >= 0 ? (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q])) : 0.0;
+    // in-lane runs: head run (may continue the previous lane), complete middle
+    // runs (emitted here), tail run (joined across lanes by the scan)
+    int head_d = dv[0];
+    double head = 0.0, run = 0.0;
+    int run_d = dv[0];
+    bool has_head = false;
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      if (dv[q] != run_d) {
+        if (!has_head) {
+          head = run;
+          has_head = true;
+        } else if (run_d >= 0) {
+          atomicAdd(acc + run_d, run);
+        }
+        run = 0.0;
+        run_d = dv[q];
+      }
+      run += v[q];
+    }
+    // segmented inclusive scan of tails (destinations nondecreasing in lane)
+    int td = run_d;
+    double tv = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      double t = __shfl_up_sync(0xffffffffu, tv, o);
+      int dd = __shfl_up_sync(0xffffffffu, td, o);
+      if (lane >= o && dd == td) tv += t;
+    }
+    const int prev_td = __shfl_up_sync(0xffffffffu, td, 1);
+    const double prev_tv = __shfl_up_sync(0xffffffffu, tv, 1);
+    const int next_head = __shfl_down_sync(0xffffffffu, head_d, 1);
+    if (has_head && head_d >= 0) {
+      double h = head;
+      if (lane > 0 && prev_td == head_d) h += prev_tv;
+      atomicAdd(acc + head_d, h);
+    }
+    // my tail is emitted by me unless the next lane continues it
+    if (td >= 0 && (lane == 31 || next_head != td)) atomicAdd(acc + td, tv);
   }
 }
 
@@ -446,10 +482,21 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   cudaStream_t st = rt.stream;
   PrBlockLayout* L = layout_for(g, pr_block_window(g, sizeof(CT), s.blocking_size), sizeof(CT));
   const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
-  DevBuf<double> rank(V), acc(V), scal(2 * (iters_cap + 2));
-  DevBuf<CT> c0(V), c1(V);
-  scal.zero(st);
-  acc.zero(st);
+  std::lock_guard<std::mutex> wlk(L->w_mu);
+  if (L->w_rank.n < (size_t)V) {
+    L->w_rank.alloc(V);
+    L->w_acc.alloc(V);
+    L->w_out.alloc(V);
+    L->w_c0.alloc(V * sizeof(CT));
+    L->w_c1.alloc(V * sizeof(CT));
+  }
+  if (L->w_scal.n < (size_t)(2 * (iters_cap + 2))) L->w_scal.alloc(2 * (iters_cap + 2));
+  struct Ptr { double* p; };
+  struct CPtr { CT* p; };
+  Ptr rank{L->w_rank.p}, acc{L->w_acc.p}, scal{L->w_scal.p}, outv{L->w_out.p};
+  CPtr c0{reinterpret_cast<CT*>(L->w_c0.p)}, c1{reinterpret_cast<CT*>(L->w_c1.p)};
+  GG_CUDA(cudaMemsetAsync(scal.p, 0, 2 * (iters_cap + 2) * sizeof(double), st));
+  GG_CUDA(cudaMemsetAsync(acc.p, 0, V * sizeof(double), st));
   k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank.p, c0.p, scal.p);
   GG_LAUNCH_CHECK();
   count_launch();
@@ -508,7 +555,6 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   }
   rt.stats.rounds += it;
   rt.stats.edges_traversed += it * g.E;
-  DevBuf<double> outv(V);
   k_unpermute<<<grid_for(V, 256, dev), 256, 0, st>>>(rank.p, L->newid.p, V, outv.p);
   GG_LAUNCH_CHECK();
   count_launch();
