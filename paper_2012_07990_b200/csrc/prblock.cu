@@ -334,7 +334,7 @@ __global__ void k_unpermute(const double* rank_new, const int32_t* newid, int64_
 template <class CT>
 __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                              int64_t e0, int64_t e1, const CT* contrib, double* acc,
-                                             int coherent) {
+                                             int coherent, const CT* s_hot = nullptr, int32_t nhot = 0) {
   // Each lane owns 8 consecutive edges (two 16-byte loads per array), so a
   // warp step covers 256 edges.  Runs of equal destination inside a lane are
   // summed in registers; runs crossing lanes are joined by ONE warp segmented
@@ -367,7 +367,9 @@ __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, co
     double v[kE];
 #pragma unroll
     for (int q = 0; q < kE; ++q)
-      v[q] = dv[q] >= 0 ? (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q])) : 0.0;
+      v[q] = dv[q] < 0 ? 0.0
+             : su[q] < nhot ? (double)s_hot[su[q]]
+             : (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q]));
     // in-lane runs: head run (may continue the previous lane), complete middle
     // runs (emitted here), tail run (joined across lanes by the scan)
     int head_d = dv[0];
@@ -414,6 +416,21 @@ template <class CT>
 static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, const int32_t* dst, int64_t e0,
                                                          int64_t e1, const CT* contrib, double* acc) {
   pr_edges_seg<CT>(src, dst, e0, e1, contrib, acc, 0);
+}
+
+// Hot segment: the first `nhot` (highest out-degree) sources' contributions
+// are staged once per CTA in shared memory; their gathers leave the L1TEX
+// tag pipeline (the bound of this kernel) for the shared-memory banks.
+constexpr int kHotThreads = 1024;
+template <class CT>
+static __global__ void __launch_bounds__(kHotThreads, 1) k_pr_edges_hot(const int32_t* src, const int32_t* dst,
+                                                                        int64_t e0, int64_t e1, const CT* contrib,
+                                                                        double* acc, int32_t nhot) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  CT* s_hot = reinterpret_cast<CT*>(s_raw);
+  for (int32_t i = threadIdx.x; i < nhot; i += blockDim.x) s_hot[i] = __ldg(contrib + i);
+  __syncthreads();
+  pr_edges_seg<CT>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
 }
 
 // vertex pass: rank' = base + d*acc, L1, next dangling mass, next contrib, acc reset.
@@ -542,6 +559,16 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   if (!fusion) {
     double l1 = INFINITY;
     const unsigned grid = (unsigned)sm_count(dev) * 8;
+    // shared-memory hot-source cache: as many top sources as fit next to the
+    // (1 CTA/SM) 1024-thread block; disabled by GG_PR_NO_SMEM_CACHE
+    int smem_max = 0;
+    GG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    int32_t nhot = (int32_t)std::min<int64_t>((smem_max - 8192) / (int)sizeof(CT), L->ns);
+    if (getenv("GG_PR_NO_SMEM_CACHE") || nhot < 1024) nhot = 0;
+    if (nhot)
+      GG_CUDA(cudaFuncSetAttribute((const void*)k_pr_edges_hot<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   nhot * (int)sizeof(CT)));
+    const unsigned hot_grid = (unsigned)sm_count(dev);
     while (!(it >= max_iters || l1 < tol)) {
       const CT* cur = (it & 1) ? c1.p : c0.p;
       CT* nxt = (it & 1) ? c0.p : c1.p;
@@ -550,7 +577,11 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
         const int64_t sg = k == L->K ? 0 : k;
         const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
         if (e1 <= e0) continue;
-        k_pr_edges<CT><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
+        if (sg == 0 && nhot > 0)
+          k_pr_edges_hot<CT><<<hot_grid, kHotThreads, nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, cur,
+                                                                             acc.p, nhot);
+        else
+          k_pr_edges<CT><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
         count_launch();
       }
       rt.edge_end();
