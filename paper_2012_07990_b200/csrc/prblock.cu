@@ -564,7 +564,8 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
     int smem_max = 0;
     GG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     int32_t nhot = (int32_t)std::min<int64_t>((smem_max - 8192) / (int)sizeof(CT), L->ns);
-    if (getenv("GG_PR_NO_SMEM_CACHE") || nhot < 1024) nhot = 0;
+    // measured slower on B200 (1 CTA/SM, speculative global loads): opt-in only
+    if (!getenv("GG_PR_SMEM_CACHE") || nhot < 1024) nhot = 0;
     if (nhot)
       GG_CUDA(cudaFuncSetAttribute((const void*)k_pr_edges_hot<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    nhot * (int)sizeof(CT)));
