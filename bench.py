@@ -31,6 +31,7 @@ CONFIGS = {
     "c5": (27, 16, 7, 20),
     "c1": (16, 16, 1, 20),
 }
+ALGO_CONFIGS = ("c2", "c3", "c4")  # bench_algos.py: BFS / SSSP / CC+BC (configs[1..3])
 
 SCHEDULES = {
     "eb": dict(load_balance="EDGE_ONLY", blocking=True),
@@ -49,7 +50,7 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="gg", choices=["gg", "reference"])
-    p.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    p.add_argument("--config", default="c5", choices=sorted(CONFIGS) + list(ALGO_CONFIGS))
     p.add_argument("--scale", type=int, default=None)
     p.add_argument("--schedule", default="eb", choices=sorted(SCHEDULES))
     p.add_argument("--fp32-contrib", action="store_true")
@@ -57,6 +58,17 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-scale", type=int, default=22)
+    # c2-c4 (bench_algos.py)
+    p.add_argument("--sources", type=int, default=None)
+    p.add_argument("--theta", type=float, default=0.05, help="c2 hybrid threshold")
+    p.add_argument("--pull-lb", default="VERTEX_BASED", help="c2 pull-side load balance")
+    p.add_argument("--fusion", action="store_true", help="c2: fused loop")
+    p.add_argument("--side", type=int, default=None, help="c3 grid side")
+    p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")
+    p.add_argument("--lb", default="ETWC", help="c3 load balance")
+    p.add_argument("--no-fusion", action="store_true", help="c3: unfused loop")
+    p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED", help="c4 load balances")
+    p.add_argument("--check", action="store_true", help="c2-c4: validate against the oracle")
     return p.parse_args()
 
 
@@ -180,6 +192,10 @@ def main():
         print(json.dumps(line))
         return
 
+    if args.config in ALGO_CONFIGS:
+        main_algo(args, metric)
+        return
+
     import numpy as np
     import torch
     import paper_2012_07990_b200 as gg
@@ -300,6 +316,25 @@ def main():
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def main_algo(args, metric):
+    """configs[1..3]: one GPU (the north star keeps BFS-DO, SSSP, CC and BC
+    single-GPU); under torchrun rank 0 runs and the other ranks exit."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    import bench_algos
+    peak, peak_kind = measured_peaks()
+    with ClockSampler(0) as clk:
+        line = bench_algos.run(args, peak, peak_kind)
+    out = {"metric": metric, "value": line.pop("value"), "unit": "GTEPS", "n_gpus": 1,
+           "steps": line.pop("steps"), "warmup": args.warmup,
+           "ms_per_step": line.pop("ms_per_step"), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": line.pop("dtype"),
+           "data": "synthetic (generated on device)"}
+    out.update(line)
+    out["clocks"] = clk.summary()
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":

@@ -331,106 +331,148 @@ __global__ void k_unpermute(const double* rank_new, const int32_t* newid, int64_
 // independent gathers per lane, then a warp segmented scan keyed by the
 // (sorted) destination so each destination run issues ONE f64 add to acc.
 // ---------------------------------------------------------------------------
-template <class CT>
+constexpr int kE = 8;  // consecutive blocked edges per lane (two 16-byte loads per array)
+
+// Load one lane's kE consecutive edges [my, my+kE) clipped to [e0, e1);
+// dst = -1 marks a dead slot.
+__device__ __forceinline__ void pr_load_edges(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                              int64_t my, int64_t e0, int64_t e1, int32_t (&su)[kE],
+                                              int32_t (&dv)[kE]) {
+  if (my + kE <= e1 && my >= e0) {
+    const int4* s4 = reinterpret_cast<const int4*>(src + my);
+    const int4* d4 = reinterpret_cast<const int4*>(dst + my);
+    int4 a0 = __ldcs(s4), a1 = __ldcs(s4 + 1), b0 = __ldcs(d4), b1 = __ldcs(d4 + 1);
+    su[0] = a0.x; su[1] = a0.y; su[2] = a0.z; su[3] = a0.w;
+    su[4] = a1.x; su[5] = a1.y; su[6] = a1.z; su[7] = a1.w;
+    dv[0] = b0.x; dv[1] = b0.y; dv[2] = b0.z; dv[3] = b0.w;
+    dv[4] = b1.x; dv[5] = b1.y; dv[6] = b1.z; dv[7] = b1.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      const int64_t e = my + q;
+      const bool live = e >= e0 && e < e1;
+      su[q] = live ? __ldcs(src + e) : 0;
+      dv[q] = live ? __ldcs(dst + e) : -1;
+    }
+  }
+}
+
+// Gather + reduce one warp step (kE*32 edges).  Runs of equal destination
+// inside a lane are summed in registers; runs crossing lanes are joined by ONE
+// warp segmented scan per step; each destination run issues one f64 add.
+// kSmem: sources < nhot are read from the CTA's shared-memory copy of the
+// hottest contributions (degree-renumbered ids: hot = small).
+template <class CT, bool kSmem>
+__device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const int32_t (&dv)[kE], const CT* contrib,
+                                               double* acc, int coherent, const CT* s_hot, int32_t nhot) {
+  const int lane = lane_id();
+  double v[kE];
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    if (kSmem)
+      v[q] = dv[q] < 0 ? 0.0
+             : su[q] < nhot ? (double)s_hot[su[q]]
+             : (double)__ldg(contrib + su[q]);
+    else
+      v[q] = dv[q] < 0 ? 0.0 : (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q]));
+  }
+  // in-lane runs: head run (may continue the previous lane), complete middle
+  // runs (emitted here), tail run (joined across lanes by the scan)
+  int head_d = dv[0];
+  double head = 0.0, run = 0.0;
+  int run_d = dv[0];
+  bool has_head = false;
+#pragma unroll
+  for (int q = 0; q < kE; ++q) {
+    if (dv[q] != run_d) {
+      if (!has_head) {
+        head = run;
+        has_head = true;
+      } else if (run_d >= 0) {
+        atomicAdd(acc + run_d, run);
+      }
+      run = 0.0;
+      run_d = dv[q];
+    }
+    run += v[q];
+  }
+  // segmented inclusive scan of tails (destinations nondecreasing in lane)
+  int td = run_d;
+  double tv = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double t = __shfl_up_sync(0xffffffffu, tv, o);
+    int dd = __shfl_up_sync(0xffffffffu, td, o);
+    if (lane >= o && dd == td) tv += t;
+  }
+  const int prev_td = __shfl_up_sync(0xffffffffu, td, 1);
+  const double prev_tv = __shfl_up_sync(0xffffffffu, tv, 1);
+  const int next_head = __shfl_down_sync(0xffffffffu, head_d, 1);
+  if (has_head && head_d >= 0) {
+    double h = head;
+    if (lane > 0 && prev_td == head_d) h += prev_tv;
+    atomicAdd(acc + head_d, h);
+  }
+  // my tail is emitted by me unless the next lane continues it
+  if (td >= 0 && (lane == 31 || next_head != td)) atomicAdd(acc + td, tv);
+}
+
+// Edge phase (EDGE_ONLY semantics, Alg. 2) over blocked edges [e0, e1) of one
+// segment: warps stride over kE*32-edge steps; the next step's edges are
+// loaded (registers) before the current step's gathers, so the DRAM latency
+// of the edge stream overlaps the L2 latency of the gathers.
+template <class CT, bool kSmem = false, bool kPrefetch = true>
 __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                              int64_t e0, int64_t e1, const CT* contrib, double* acc,
                                              int coherent, const CT* s_hot = nullptr, int32_t nhot = 0) {
-  // Each lane owns 8 consecutive edges (two 16-byte loads per array), so a
-  // warp step covers 256 edges.  Runs of equal destination inside a lane are
-  // summed in registers; runs crossing lanes are joined by ONE warp segmented
-  // scan per step (instead of one per 32 edges).
-  constexpr int kE = 8;
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t start = e0 & ~int64_t(kE - 1);  // 32-byte aligned start
-  for (int64_t base = start + warp * 32 * kE; base < e1; base += nwarps * 32 * kE) {
-    const int64_t my = base + lane * kE;
-    int32_t su[kE], dv[kE];
-    if (my + kE <= e1 && my >= e0) {
-      const int4* s4 = reinterpret_cast<const int4*>(src + my);
-      const int4* d4 = reinterpret_cast<const int4*>(dst + my);
-      int4 a0 = __ldcs(s4), a1 = __ldcs(s4 + 1), b0 = __ldcs(d4), b1 = __ldcs(d4 + 1);
-      su[0] = a0.x; su[1] = a0.y; su[2] = a0.z; su[3] = a0.w;
-      su[4] = a1.x; su[5] = a1.y; su[6] = a1.z; su[7] = a1.w;
-      dv[0] = b0.x; dv[1] = b0.y; dv[2] = b0.z; dv[3] = b0.w;
-      dv[4] = b1.x; dv[5] = b1.y; dv[6] = b1.z; dv[7] = b1.w;
-    } else {
-#pragma unroll
-      for (int q = 0; q < kE; ++q) {
-        const int64_t e = my + q;
-        const bool live = e >= e0 && e < e1;
-        su[q] = live ? __ldcs(src + e) : 0;
-        dv[q] = live ? __ldcs(dst + e) : -1;
-      }
+  const int64_t stride = nwarps * 32 * kE;
+  int64_t base = start + warp * 32 * kE;
+  if (base >= e1) return;
+  int32_t su[kE], dv[kE];
+  pr_load_edges(src, dst, base + lane * kE, e0, e1, su, dv);
+  for (; base < e1; base += stride) {
+    if (!kPrefetch) {
+      if (base != start + warp * 32 * kE) pr_load_edges(src, dst, base + lane * kE, e0, e1, su, dv);
+      pr_reduce_step<CT, kSmem>(su, dv, contrib, acc, coherent, s_hot, nhot);
+      continue;
     }
-    double v[kE];
-#pragma unroll
-    for (int q = 0; q < kE; ++q)
-      v[q] = dv[q] < 0 ? 0.0
-             : su[q] < nhot ? (double)s_hot[su[q]]
-             : (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q]));
-    // in-lane runs: head run (may continue the previous lane), complete middle
-    // runs (emitted here), tail run (joined across lanes by the scan)
-    int head_d = dv[0];
-    double head = 0.0, run = 0.0;
-    int run_d = dv[0];
-    bool has_head = false;
+    int32_t nsu[kE], ndv[kE];
+    pr_load_edges(src, dst, base + stride + lane * kE, e0, e1, nsu, ndv);  // dead past e1
+    pr_reduce_step<CT, kSmem>(su, dv, contrib, acc, coherent, s_hot, nhot);
 #pragma unroll
     for (int q = 0; q < kE; ++q) {
-      if (dv[q] != run_d) {
-        if (!has_head) {
-          head = run;
-          has_head = true;
-        } else if (run_d >= 0) {
-          atomicAdd(acc + run_d, run);
-        }
-        run = 0.0;
-        run_d = dv[q];
-      }
-      run += v[q];
+      su[q] = nsu[q];
+      dv[q] = ndv[q];
     }
-    // segmented inclusive scan of tails (destinations nondecreasing in lane)
-    int td = run_d;
-    double tv = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      double t = __shfl_up_sync(0xffffffffu, tv, o);
-      int dd = __shfl_up_sync(0xffffffffu, td, o);
-      if (lane >= o && dd == td) tv += t;
-    }
-    const int prev_td = __shfl_up_sync(0xffffffffu, td, 1);
-    const double prev_tv = __shfl_up_sync(0xffffffffu, tv, 1);
-    const int next_head = __shfl_down_sync(0xffffffffu, head_d, 1);
-    if (has_head && head_d >= 0) {
-      double h = head;
-      if (lane > 0 && prev_td == head_d) h += prev_tv;
-      atomicAdd(acc + head_d, h);
-    }
-    // my tail is emitted by me unless the next lane continues it
-    if (td >= 0 && (lane == 31 || next_head != td)) atomicAdd(acc + td, tv);
   }
 }
 
-template <class CT>
+template <class CT, bool kPrefetch>
 static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, const int32_t* dst, int64_t e0,
                                                          int64_t e1, const CT* contrib, double* acc) {
-  pr_edges_seg<CT>(src, dst, e0, e1, contrib, acc, 0);
+  pr_edges_seg<CT, false, kPrefetch>(src, dst, e0, e1, contrib, acc, 0);
 }
 
 // Hot segment: the first `nhot` (highest out-degree) sources' contributions
 // are staged once per CTA in shared memory; their gathers leave the L1TEX
-// tag pipeline (the bound of this kernel) for the shared-memory banks.
-constexpr int kHotThreads = 1024;
-template <class CT>
-static __global__ void __launch_bounds__(kHotThreads, 1) k_pr_edges_hot(const int32_t* src, const int32_t* dst,
-                                                                        int64_t e0, int64_t e1, const CT* contrib,
-                                                                        double* acc, int32_t nhot) {
+// line pipeline and the L2 (the two bounds of this kernel, ~1 line/clk/SM)
+// for the shared-memory banks.
+template <class CT, int kThreads, int kMinBlocks>
+static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(const int32_t* src, const int32_t* dst,
+                                                                             int64_t e0, int64_t e1, const CT* contrib,
+                                                                             double* acc, int32_t nhot) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   CT* s_hot = reinterpret_cast<CT*>(s_raw);
-  for (int32_t i = threadIdx.x; i < nhot; i += blockDim.x) s_hot[i] = __ldg(contrib + i);
+  const int n4 = (int)((int64_t)nhot * sizeof(CT) / 16);
+  for (int i = threadIdx.x; i < n4; i += blockDim.x)
+    reinterpret_cast<int4*>(s_raw)[i] = __ldg(reinterpret_cast<const int4*>(contrib) + i);
+  for (int i = n4 * (16 / (int)sizeof(CT)) + threadIdx.x; i < nhot; i += blockDim.x) s_hot[i] = __ldg(contrib + i);
   __syncthreads();
-  pr_edges_seg<CT>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
+  pr_edges_seg<CT, true>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
 }
 
 // vertex pass: rank' = base + d*acc, L1, next dangling mass, next contrib, acc reset.
@@ -559,17 +601,29 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   if (!fusion) {
     double l1 = INFINITY;
     const unsigned grid = (unsigned)sm_count(dev) * 8;
-    // shared-memory hot-source cache: as many top sources as fit next to the
-    // (1 CTA/SM) 1024-thread block; disabled by GG_PR_NO_SMEM_CACHE
+    // shared-memory hot-source cache for the hot segment: the top `nhot`
+    // sources (as many as fit next to the CTA).  GG_PR_HOT=0 disables it,
+    // GG_PR_HOT_THREADS picks 1024x1 (default) or 512x2 CTAs per SM,
+    // GG_PR_NHOT caps the cached count.
     int smem_max = 0;
     GG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    int32_t nhot = (int32_t)std::min<int64_t>((smem_max - 8192) / (int)sizeof(CT), L->ns);
-    // measured slower on B200 (1 CTA/SM, speculative global loads): opt-in only
-    if (!getenv("GG_PR_SMEM_CACHE") || nhot < 1024) nhot = 0;
+    const char* hot_env = getenv("GG_PR_HOT");
+    const bool hot_on = !(hot_env && atoi(hot_env) == 0);
+    const char* thr_env = getenv("GG_PR_HOT_THREADS");
+    const int hot_threads = thr_env && atoi(thr_env) == 512 ? 512 : 1024;
+    const int per_sm = hot_threads == 512 ? 2 : 1;
+    int smem_per_cta = smem_max - 2048;
+    if (per_sm == 2) smem_per_cta = (smem_max - 4096) / 2;
+    int64_t nhot64 = std::min<int64_t>(smem_per_cta / (int)sizeof(CT), L->ns);
+    if (const char* nh = getenv("GG_PR_NHOT")) nhot64 = std::min<int64_t>(nhot64, atoll(nh));
+    nhot64 &= ~int64_t(3);
+    int32_t nhot = hot_on && nhot64 >= 1024 ? (int32_t)nhot64 : 0;
+    const void* hot_fn = per_sm == 2 ? (const void*)k_pr_edges_hot<CT, 512, 2> : (const void*)k_pr_edges_hot<CT, 1024, 1>;
     if (nhot)
-      GG_CUDA(cudaFuncSetAttribute((const void*)k_pr_edges_hot<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   nhot * (int)sizeof(CT)));
-    const unsigned hot_grid = (unsigned)sm_count(dev);
+      GG_CUDA(cudaFuncSetAttribute(hot_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, nhot * (int)sizeof(CT)));
+    const unsigned hot_grid = (unsigned)sm_count(dev) * per_sm;
+    const char* pf_env = getenv("GG_PR_PREFETCH");  // register prefetch of the next edge step
+    const bool prefetch = !(pf_env && atoi(pf_env) == 0);
     while (!(it >= max_iters || l1 < tol)) {
       const CT* cur = (it & 1) ? c1.p : c0.p;
       CT* nxt = (it & 1) ? c0.p : c1.p;
@@ -578,11 +632,16 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
         const int64_t sg = k == L->K ? 0 : k;
         const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
         if (e1 <= e0) continue;
-        if (sg == 0 && nhot > 0)
-          k_pr_edges_hot<CT><<<hot_grid, kHotThreads, nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, cur,
+        if (sg == 0 && nhot > 0 && per_sm == 2)
+          k_pr_edges_hot<CT, 512, 2><<<hot_grid, 512, nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, cur,
                                                                              acc.p, nhot);
+        else if (sg == 0 && nhot > 0)
+          k_pr_edges_hot<CT, 1024, 1><<<hot_grid, 1024, nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, cur,
+                                                                               acc.p, nhot);
+        else if (prefetch)
+          k_pr_edges<CT, true><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
         else
-          k_pr_edges<CT><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
+          k_pr_edges<CT, false><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
         count_launch();
       }
       rt.edge_end();
