@@ -10,8 +10,10 @@ graph resident in HBM; metric GTEPS = 20*E / step time.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gg|reference]
                   [--config c5|c1|...] [--scale S] [--schedule eb|edge|pull|...]
 
-Multi-GPU (torchrun): every rank runs the same per-GPU workload on its own
-device ("scaling": "weak", replicas); value = all ranks' edges / max time.
+Multi-GPU (torchrun): the same RMAT-27 graph is 1-D partitioned by
+destination over the N ranks (EdgeBlocking layout per rank, NCCL allgather of
+contributions every iteration; "scaling": "strong"); value = 20*E / max over
+ranks of the step time.
 """
 
 import argparse
@@ -163,11 +165,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    metric = "GTEPS per algorithm x graph (PR/BFS/SSSP/CC/BC); PR GTEPS at 1/2/4/8 GPUs"
+    if args.config in ALGO_CONFIGS:
+        main_algo(args, metric)
+        return
     scale, ef, seed, iters = CONFIGS[args.config]
     if args.scale:
         scale = args.scale
     workload = "pagerank_%s_rmat%d_ef%d" % (args.schedule, scale, ef)
-    metric = "GTEPS per algorithm x graph (PR/BFS/SSSP/CC/BC); PR GTEPS at 1/2/4/8 GPUs"
 
     if args.impl == "reference":
         if rank != 0:
@@ -190,10 +195,6 @@ def main():
                 "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
-        return
-
-    if args.config in ALGO_CONFIGS:
-        main_algo(args, metric)
         return
 
     import numpy as np
@@ -221,16 +222,30 @@ def main():
     import ctypes as C
     from paper_2012_07990_b200 import _lib
     from paper_2012_07990_b200.engine import binding_pod
-    pm = C.c_double()
-    pod = binding_pod(sch)
-    _lib.call("gg_pagerank_prepare", g.handle, C.byref(pod), 1 if args.fp32_contrib else 0,
-              C.byref(pm))
-    prep_ms = pm.value
     ranks = torch.empty(V, dtype=torch.float64, device="cuda")
+    comm = None
+    if world > 1:
+        # N > 1: the graph is 1-D partitioned by destination (renumbered ids,
+        # balanced by in-edges); every rank generates the same RMAT graph,
+        # keeps its own destinations' in-edges, and allgathers contributions
+        # over NCCL each iteration (strong scaling: total work fixed).
+        from paper_2012_07990_b200.dist import Comm, pagerank_dist, prepare_dist
+        comm = Comm.create(rank, world, local)
+        prep_ms = prepare_dist(world, rank, g, prog, contrib_fp32=args.fp32_contrib)
 
-    def step():
-        return gg.pagerank(g, prog, max_iters=iters, tolerance=0.0, out=ranks,
-                           contrib_fp32=args.fp32_contrib)
+        def step():
+            return pagerank_dist(comm, g, max_iters=iters, tolerance=0.0, out=ranks,
+                                 program=prog, contrib_fp32=args.fp32_contrib)[1]
+    else:
+        pm = C.c_double()
+        pod = binding_pod(sch)
+        _lib.call("gg_pagerank_prepare", g.handle, C.byref(pod), 1 if args.fp32_contrib else 0,
+                  C.byref(pm))
+        prep_ms = pm.value
+
+        def step():
+            return gg.pagerank(g, prog, max_iters=iters, tolerance=0.0, out=ranks,
+                               contrib_fp32=args.fp32_contrib).stats
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -243,11 +258,13 @@ def main():
         edge_ms = 0.0
         edge_n = 0
         launches = 0
+        e_local = 0
         for _ in range(args.steps):
-            r = step()
-            edge_ms += r.stats.edge_ms
-            edge_n += r.stats.edge_launches
-            launches += r.stats.gpu_launches
+            st = step()
+            edge_ms += st.edge_ms
+            edge_n += st.edge_launches
+            launches += st.gpu_launches
+            e_local = st.edges_traversed // iters
         ev1.record()
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -255,24 +272,28 @@ def main():
     if dist is not None:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    value = world * iters * E / (ms * 1e-3) / 1e9
+    # strong scaling: the same RMAT-27 graph at every N (partitioned at N > 1)
+    value = iters * E / (ms * 1e-3) / 1e9
 
     # roofline of the dominant kernel (edge phase), algorithmic bytes per launch:
     # 8 B/edge (COO pair) + 16 B/vertex (contrib read, acc write) -- SURVEY §8(d)
     avg_edge_ms = edge_ms / max(1, edge_n)
-    alg_edge = 8.0 * E + 16.0 * V
+    alg_edge = 8.0 * e_local + 16.0 * V / world  # this rank's share (all of it at N=1)
     achieved = alg_edge / (avg_edge_ms * 1e-3) / 1e9
     alg_iter = 8.0 * E + 32.0 * V
-    iter_achieved = alg_iter * iters / (ms * 1e-3) / 1e9
+    iter_achieved = alg_iter * iters / (ms * 1e-3) / 1e9 / world  # per-GPU share of the aggregate
 
     line = {"metric": metric, "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" + ("(contrib f32)" if args.fp32_contrib else ""),
             "data": "synthetic RMAT generated on device (sort_by_source%s)"
                     % (", permuted ids" if args.permute else ", natural ids"),
             "config": {"workload": workload, "V": V, "E": E, "iterations": iters,
                        "schedule": SCHEDULES[args.schedule], "blocking_prep_ms": prep_ms,
+                       "parallelism": ("1-D destination partition x%d, NCCL allgather of "
+                                       "contributions per iteration" % world) if world > 1
+                                      else "single GPU",
                        "generate_s": gen_s,
                        "l2": "inputs (%.1f GB) larger than L2; no flush needed" % (8 * E / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -296,8 +317,12 @@ def main():
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             ge = gg.Graph.from_coo(V, src_h.numpy(), dst_h.numpy(), device=local)
-            gg.pagerank(ge, prog, max_iters=iters, tolerance=0.0, out=ranks_h.numpy(),
-                        contrib_fp32=args.fp32_contrib)
+            if comm is not None:
+                pagerank_dist(comm, ge, max_iters=iters, tolerance=0.0, out=ranks_h.numpy(),
+                              program=prog, contrib_fp32=args.fp32_contrib)
+            else:
+                gg.pagerank(ge, prog, max_iters=iters, tolerance=0.0, out=ranks_h.numpy(),
+                            contrib_fp32=args.fp32_contrib)
             ge.close()
         barrier()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
@@ -305,7 +330,7 @@ def main():
         if dist is not None:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e_s = float(e2e_t.item())
-        line["e2e"] = {"value": world * iters * E / e2e_s / 1e9, "unit": "GTEPS",
+        line["e2e"] = {"value": iters * E / e2e_s / 1e9, "unit": "GTEPS",
                        "h2d_bytes_per_step": 8 * E, "d2h_bytes_per_step": 8 * V,
                        "s_per_step": e2e_s,
                        "includes": "H2D of COO from pinned host memory, device graph build "
@@ -314,6 +339,8 @@ def main():
         line["cpu_baseline"] = cpu_pagerank_sample(min(args.cpu_scale, scale), ef, seed)
     if rank == 0:
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -241,6 +241,23 @@ int gg_comm_destroy(gg_comm* c);
 int gg_pagerank_dist(gg_comm* c, const gg_graph* g, int64_t max_iters, double tolerance,
                      double damping, double* ranks /* V, gathered on every rank */,
                      gg_stats* stats);
+/* The same with the bound schedule: EDGE_ONLY + BLOCKED runs the
+ * EdgeBlocking layout over this rank's destinations (renumbered ids,
+ * partition balanced by in-edges), any other schedule the PULL gather above.
+ * Replaces blocking.apply_blocked (blocking.py:116-186) driven by
+ * algos.pagerank (algos.py:163-208) for one partition of a multi-GPU run. */
+int gg_pagerank_dist_ex(gg_comm* c, const gg_graph* g, const gg_binding* binding,
+                        int32_t fp32_contrib, int64_t max_iters, double tolerance, double damping,
+                        double* ranks, gg_stats* stats);
+/* Build (and cache) rank `rank` of `nranks`'s layout without running. */
+int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g,
+                             const gg_binding* binding, int32_t fp32_contrib, double* prep_ms);
+/* Test mode of the partitioned run: `nparts` virtual ranks on the graph's
+ * one device, each with its own layout and buffers, exchanging by copies in
+ * the same order as the NCCL exchange.  EDGE_ONLY + BLOCKED only. */
+int gg_pagerank_virtual(const gg_graph* g, int32_t nparts, const gg_binding* binding,
+                        int32_t fp32_contrib, int64_t max_iters, double tolerance, double damping,
+                        double* ranks, gg_stats* stats);
 
 #ifdef __cplusplus
 }

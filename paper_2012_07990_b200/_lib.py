@@ -121,6 +121,12 @@ SIGNATURES = {
     "gg_comm_init": (I32, [I32, I32, I32, VP, PP]),
     "gg_comm_destroy": (I32, [VP]),
     "gg_pagerank_dist": (I32, [VP, VP, I64, F64, F64, VP, C.POINTER(GGStats)]),
+    "gg_pagerank_dist_ex": (I32, [VP, VP, C.POINTER(GGBinding), I32, I64, F64, F64, VP,
+                                  C.POINTER(GGStats)]),
+    "gg_pagerank_dist_prepare": (I32, [I32, I32, VP, C.POINTER(GGBinding), I32,
+                                       C.POINTER(F64)]),
+    "gg_pagerank_virtual": (I32, [VP, I32, C.POINTER(GGBinding), I32, I64, F64, F64, VP,
+                                  C.POINTER(GGStats)]),
 }
 
 _lib = None

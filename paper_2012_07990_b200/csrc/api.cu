@@ -1,6 +1,7 @@
 // api.cu — the extern "C" boundary (include/gg.h).  Every entry point catches
 // library exceptions and maps them to gg_status codes + gg_last_error().
 #include "engine.cuh"
+#include "prdist.cuh"
 #include <cstring>
 
 namespace gg {
@@ -45,6 +46,8 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
 int64_t pagerank_dist_run(gg_comm* c, const Graph& g, int64_t max_iters, double tol, double damping,
                           double* ranks_out, Runtime& rt);
 double pr_block_prep_ms(const Graph& g, int64_t blocking_size, int ct_bytes);
+int64_t pagerank_dist_blocked(gg_comm* c, const Graph& g, const gg_schedule& s, bool fp32, int64_t max_iters,
+                              double tol, double damping, double* ranks_out, Runtime& rt);
 inline void pr_block_prep(const Graph& g, int64_t blocking_size, int ct_bytes) {
   pr_block_prep_ms(g, blocking_size, ct_bytes);
 }
@@ -533,6 +536,69 @@ int gg_pagerank_dist(gg_comm* c, const gg_graph* g, int64_t max_iters, double to
   Runtime rt(g->g.get(), nullptr);
   CallTimer t(g->g->dev);
   pagerank_dist_run(c, *g->g, max_iters, tolerance, damping, ranks, rt);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_pagerank_dist_ex(gg_comm* c, const gg_graph* g, const gg_binding* binding, int32_t fp32_contrib,
+                        int64_t max_iters, double tolerance, double damping, double* ranks, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(c);
+  NEED(g);
+  NEED(binding);
+  NEED(ranks);
+  check_binding(*binding);
+  if (binding->is_hybrid) fail(GG_ERR_SCHEDULE, "label 's0:s1' of pagerank takes a SimpleGPUSchedule");
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), nullptr);
+  CallTimer t(g->g->dev);
+  const gg_schedule& s = binding->s1;
+  if (s.load_balance == GG_LB_EDGE_ONLY && s.blocking)
+    pagerank_dist_blocked(c, *g->g, s, fp32_contrib != 0, max_iters, tolerance, damping, ranks, rt);
+  else
+    pagerank_dist_run(c, *g->g, max_iters, tolerance, damping, ranks, rt);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g, const gg_binding* binding,
+                             int32_t fp32_contrib, double* prep_ms) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  check_binding(*binding);
+  if (nranks < 1 || rank < 0 || rank >= nranks) fail(GG_ERR_VALUE, "bad rank/nranks");
+  DeviceGuard guard(g->g->dev);
+  double t0 = now_ms();
+  const gg_schedule& s = binding->s1;
+  if (s.load_balance == GG_LB_EDGE_ONLY && s.blocking)
+    pr_block_prep_part_ms(*g->g, s.blocking_size, fp32_contrib ? 4 : 8, nranks, rank);
+  else {
+    g->g->out_view();
+    g->g->in_view();
+  }
+  GG_CUDA(cudaDeviceSynchronize());
+  if (prep_ms) *prep_ms = now_ms() - t0;
+  GG_API_END
+}
+
+int gg_pagerank_virtual(const gg_graph* g, int32_t nparts, const gg_binding* binding, int32_t fp32_contrib,
+                        int64_t max_iters, double tolerance, double damping, double* ranks, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  NEED(ranks);
+  check_binding(*binding);
+  const gg_schedule& s = binding->s1;
+  if (binding->is_hybrid || !(s.load_balance == GG_LB_EDGE_ONLY && s.blocking))
+    fail(GG_ERR_SCHEDULE, "virtual-rank PageRank runs the EdgeBlocking schedule (EDGE_ONLY + BLOCKED)");
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), nullptr);
+  CallTimer t(g->g->dev);
+  if (fp32_contrib)
+    pagerank_blocked_virtual<float>(*g->g, s, nparts, max_iters, tolerance, damping, ranks, rt);
+  else
+    pagerank_blocked_virtual<double>(*g->g, s, nparts, max_iters, tolerance, damping, ranks, rt);
   t.finish(g->g->dev, rt, stats);
   GG_API_END
 }

@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include "prpull.cuh"
+#include "prdist.cuh"
 
 namespace gg {
 
@@ -144,6 +145,39 @@ int gg_comm_destroy(gg_comm* c) {
 }
 
 namespace gg {
+// NCCL exchange of the partitioned EdgeBlocking run (prdist.cuh): one rank
+// per process; the slices have unequal lengths, so the all-gather is a group
+// of in-place broadcasts (one per owner).
+struct NcclExchange : PrExchange {
+  gg_comm* c;
+  explicit NcclExchange(gg_comm* cc) : c(cc) {}
+  void allreduce2(std::vector<double*>& d, cudaStream_t st) override {
+    NcclApi& api = nccl();
+    GG_NCCL(api.AllReduce(d[0], d[0], 2, ncclFloat64, ncclSum, c->comm, st));
+  }
+  void allgather(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                 cudaStream_t st) override {
+    NcclApi& api = nccl();
+    GG_NCCL(api.GroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+      const size_t cnt = (size_t)(bounds[r + 1] - bounds[r]) * elt;
+      char* p = (char*)bufs[0] + (size_t)bounds[r] * elt;
+      if (cnt) GG_NCCL(api.Broadcast(p, p, cnt, ncclUint8, r, c->comm, st));
+    }
+    GG_NCCL(api.GroupEnd());
+  }
+};
+
+int64_t pagerank_dist_blocked(gg_comm* c, const Graph& g, const gg_schedule& s, bool fp32, int64_t max_iters,
+                              double tol, double damping, double* ranks_out, Runtime& rt) {
+  NcclExchange ex(c);
+  int64_t local = 0;
+  if (fp32)
+    pagerank_blocked_rank<float>(g, s, c->nranks, c->rank, ex, max_iters, tol, damping, ranks_out, rt, &local);
+  else
+    pagerank_blocked_rank<double>(g, s, c->nranks, c->rank, ex, max_iters, tol, damping, ranks_out, rt, &local);
+  return local;
+}
 int64_t pagerank_dist_run(gg_comm* c, const Graph& g, int64_t max_iters, double tol, double damping,
                           double* ranks_out, Runtime& rt);
 }

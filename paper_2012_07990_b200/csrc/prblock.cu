@@ -27,6 +27,7 @@
 // back on output.  Results equal the reference's up to f64 summation order.
 #include "prtile.cuh"
 #include "apply.cuh"
+#include "prdist.cuh"
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/device/device_scan.cuh>
@@ -35,22 +36,25 @@
 
 namespace gg {
 
-struct TileSeg {
-  const int64_t* tile_row;
-  const int64_t* tile_edge;
-  int64_t ntiles;
+// Destination partition of a multi-GPU run: this rank owns the
+// renumbered destinations [lo, hi); P == 1 owns everything.
+struct PrPart {
+  int P = 1, r = 0;
 };
 
 struct PrBlockLayout {
   int64_t ns = 0, K = 0, V = 0, E = 0, nrows = 0;
   int ct_bytes = 0;
+  int P = 1, r = 0;
+  int64_t lo = 0, hi = 0;                            // owned destinations (renumbered ids)
+  std::vector<int64_t> bounds;                       // P+1 partition bounds (renumbered ids)
   DevBuf<int32_t> newid, order, outdeg, src, owner;  // owner: cold pair -> destination
-  DevBuf<int32_t> dst;                               // destination of every blocked edge
+  DevBuf<int32_t> dst;                               // local destination of every blocked edge
   std::vector<int64_t> seg_edge;                     // K+1 edge boundaries (segment 0 = hot)
-  DevBuf<int64_t> roff;                              // all rows: hot [0,V) then cold pairs
+  DevBuf<int64_t> roff;                              // all rows: hot [0,Vloc) then cold pairs
   std::vector<int64_t> seg_row;                      // K+1 row boundaries (segment 0 = hot)
-  std::vector<TilePlan> tiles;                       // per segment
   double prep_ms = 0;
+  int64_t vloc() const { return hi - lo; }
   // per-run work buffers, kept across calls (cudaMalloc/cudaFree of GB-sized
   // buffers per call would dominate short runs)
   DevBuf<double> w_rank, w_acc, w_scal, w_out;
@@ -80,14 +84,43 @@ __global__ void k_relabel_tables(const int32_t* order, const int64_t* off, int64
     outdeg_new[i] = (int32_t)(off[o + 1] - off[o]);
   }
 }
+// key = (source segment, local destination, source); edges whose
+// destination another rank owns get segment K (sorted past every kept edge).
 __global__ void k_edge_keys(const int32_t* s, const int32_t* d, int64_t E, const int32_t* newid,
-                            int64_t ns, int nvb, uint64_t* key) {
+                            int64_t ns, int nvb, int64_t lo, int64_t hi, uint64_t K, uint64_t* key) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t nu = (uint32_t)newid[s[e]], nv = (uint32_t)newid[d[e]];
+    uint64_t nu = (uint32_t)newid[s[e]];
+    int64_t nv = newid[d[e]];
+    if (nv < lo || nv >= hi) {
+      key[e] = K << (32 + nvb);
+      continue;
+    }
     uint64_t k = nu / (uint64_t)ns;
-    key[e] = (k << (32 + nvb)) | (nv << 32) | nu;
+    key[e] = (k << (32 + nvb)) | ((uint64_t)(nv - lo) << 32) | nu;
   }
+}
+// in-degree per renumbered vertex (partition balance)
+__global__ void k_indeg_new(const int32_t* d, int64_t E, const int32_t* newid, unsigned long long* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + newid[d[e]], 1ULL);
+}
+// bounds[r] = first renumbered v (rounded down to a multiple of 32, so the
+// vertex pass keeps 16-byte alignment) with in_off[v] >= r*E/P
+__global__ void k_part_bounds(const unsigned long long* in_off, int64_t V, int P, int64_t* bounds) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > P) return;
+  if (r == 0) { bounds[0] = 0; return; }
+  if (r == P) { bounds[r] = V; return; }
+  const unsigned long long E = in_off[V];
+  const unsigned long long target = (unsigned long long)((unsigned __int128)E * r / P);
+  int64_t lo = 0, hi = V;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (in_off[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  bounds[r] = lo & ~int64_t(31);
 }
 __global__ void k_split_keys(const uint64_t* key, int64_t E, int nvb, int32_t* src, int32_t* dst_hot,
                              int64_t E0) {
@@ -142,32 +175,6 @@ static T dget(const T* p) {
   return h;
 }
 
-static void plan_tiles(const int64_t* roff, int64_t row0, int64_t nrows, int64_t nedges, int dev,
-                       TilePlan& tp, bool want_cross) {
-  tp.nrows = nrows;
-  tp.ntiles = (nrows + nedges + kTile - 1) / kTile;
-  tp.tile_row.alloc(tp.ntiles + 1);
-  tp.tile_edge.alloc(tp.ntiles + 1);
-  k_tile_starts<<<grid_for(tp.ntiles + 1, 256, dev), 256>>>(roff, nrows, row0, tp.ntiles, tp.tile_row.p,
-                                                              tp.tile_edge.p);
-  GG_LAUNCH_CHECK();
-  if (!want_cross) return;
-  DevBuf<uint8_t> mark(nrows + 1);
-  mark.zero();
-  if (tp.ntiles > 1)
-    k_mark_cross<<<grid_for(tp.ntiles, 256, dev), 256>>>(roff, tp.tile_row.p, tp.tile_edge.p, tp.ntiles,
-                                                         row0, nrows, mark.p);
-  GG_LAUNCH_CHECK();
-  tp.cross.alloc(nrows + 1);
-  DevBuf<unsigned long long> n(1);
-  cub::CountingInputIterator<int32_t> it((int32_t)0);
-  size_t temp = 0;
-  GG_CUDA(cub::DeviceSelect::Flagged(nullptr, temp, it, mark.p, tp.cross.p, n.p, nrows));
-  DevBuf<uint8_t> tb(temp);
-  GG_CUDA(cub::DeviceSelect::Flagged(tb.p, temp, it, mark.p, tp.cross.p, n.p, nrows));
-  tp.ncross = (int64_t)dget(n.p);
-}
-
 __global__ void k_pair_owner(const uint64_t* key, const int64_t* pstart, int64_t n, int nvb, int32_t* owner) {
   const uint64_t mask = (1ULL << nvb) - 1;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
@@ -175,9 +182,9 @@ __global__ void k_pair_owner(const uint64_t* key, const int64_t* pstart, int64_t
     owner[p] = (int32_t)((key[pstart[p]] >> 32) & mask);
 }
 
-static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, int ct_bytes) {
+static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, int ct_bytes, PrPart part) {
   const int dev = g.dev;
-  const int64_t V = g.V, E = g.E;
+  const int64_t V = g.V, Eall = g.E;
   if (!g.has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
   CsrView out = g.out_view();
   auto L = std::make_shared<PrBlockLayout>();
@@ -185,11 +192,9 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   L->ns = ns;
   L->K = (V + ns - 1) / ns;
   L->V = V;
-  L->E = E;
   L->ct_bytes = ct_bytes;
-  const int nvb = nbits((uint64_t)(V > 1 ? V - 1 : 1));
-  const int kb = nbits((uint64_t)(L->K > 1 ? L->K - 1 : 1));
-  if (32 + nvb + kb > 64) fail(GG_ERR_VALUE, "EdgeBlocking layout: too many segments for this graph");
+  L->P = part.P;
+  L->r = part.r;
   // 1. out-degree renumbering (stable, descending)
   {
     DevBuf<uint32_t> key(V), key2(V);
@@ -206,16 +211,45 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
     k_relabel_tables<<<grid_for(V, 256, dev), 256>>>(L->order.p, out.off, V, L->newid.p, L->outdeg.p);
     GG_LAUNCH_CHECK();
   }
-  // 2-3. (segment, dst, src) keys, sorted
-  DevBuf<uint64_t> keys(E);
-  {
-    DevBuf<uint64_t> k0(E);
-    k_edge_keys<<<grid_for(E, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, E, L->newid.p, ns, nvb, k0.p);
+  // 1b. destination partition in the renumbered id space, balanced by in-edges
+  L->bounds.assign(part.P + 1, 0);
+  L->bounds[part.P] = V;
+  int64_t E = Eall;  // edges this rank keeps
+  if (part.P > 1) {
+    DevBuf<unsigned long long> cnt(V + 1), off(V + 1);
+    cnt.zero();
+    k_indeg_new<<<grid_for(Eall, 256, dev), 256>>>(g.coo_dst.p, Eall, L->newid.p, cnt.p);
     GG_LAUNCH_CHECK();
     size_t temp = 0;
-    GG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, k0.p, keys.p, E, 0, 32 + nvb + kb));
+    GG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, cnt.p, off.p, V + 1));
     DevBuf<uint8_t> tb(temp);
-    GG_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, temp, k0.p, keys.p, E, 0, 32 + nvb + kb));
+    GG_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, temp, cnt.p, off.p, V + 1));
+    DevBuf<int64_t> db(part.P + 1);
+    k_part_bounds<<<1, 256>>>(off.p, V, part.P, db.p);
+    GG_LAUNCH_CHECK();
+    GG_CUDA(cudaMemcpy(L->bounds.data(), db.p, (part.P + 1) * 8, cudaMemcpyDeviceToHost));
+    const int64_t elo = (int64_t)dget(off.p + L->bounds[part.r]);
+    const int64_t ehi = (int64_t)dget(off.p + L->bounds[part.r + 1]);
+    E = ehi - elo;
+  }
+  L->lo = L->bounds[part.r];
+  L->hi = L->bounds[part.r + 1];
+  L->E = E;
+  const int64_t Vl = L->hi - L->lo;
+  const int nvb = nbits((uint64_t)(Vl > 1 ? Vl - 1 : 1));
+  const int kb = nbits((uint64_t)L->K);  // segment K marks edges of other ranks
+  if (32 + nvb + kb > 64) fail(GG_ERR_VALUE, "EdgeBlocking layout: too many segments for this graph");
+  // 2-3. (segment, dst, src) keys, sorted; other ranks' edges sort last
+  DevBuf<uint64_t> keys(Eall);
+  {
+    DevBuf<uint64_t> k0(Eall);
+    k_edge_keys<<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, Eall, L->newid.p, ns, nvb, L->lo,
+                                                   L->hi, (uint64_t)L->K, k0.p);
+    GG_LAUNCH_CHECK();
+    size_t temp = 0;
+    GG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, k0.p, keys.p, Eall, 0, 32 + nvb + kb));
+    DevBuf<uint8_t> tb(temp);
+    GG_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, temp, k0.p, keys.p, Eall, 0, 32 + nvb + kb));
   }
   const int shift = 32 + nvb;
   DevBuf<unsigned long long> cnt(1);
@@ -223,8 +257,8 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   k_count_hot<<<grid_for(E, 256, dev), 256>>>(keys.p, E, shift, cnt.p);
   GG_LAUNCH_CHECK();
   const int64_t E0 = (int64_t)dget(cnt.p);
-  // 4. rows: [0, V) hot destinations (CSR over the hot edges), then the cold
-  //    (segment, destination) pairs; one offsets array for all rows.
+  // 4. rows: [0, Vl) hot (local) destinations (CSR over the hot edges), then
+  //    the cold (segment, destination) pairs; one offsets array for all rows.
   L->src.alloc(E);
   L->dst.alloc(E);
   k_dst_of_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->dst.p);
@@ -243,26 +277,26 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
     GG_CUDA(cub::DeviceSelect::If(tb.p, temp, it, pstart.p, npairs.p, Ec, pred));
     P = (int64_t)dget(npairs.p);
   }
-  L->nrows = V + P;
-  L->roff.alloc(V + P + 1);
+  L->nrows = Vl + P;
+  L->roff.alloc(Vl + P + 1);
   {
     DevBuf<int32_t> dh(E0 > 0 ? E0 : 1);
     k_split_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->src.p, dh.p, E0);
     GG_LAUNCH_CHECK();
-    offsets_from_sorted(dev, dh.p, E0, V, L->roff.p, 0);  // roff[0..V], roff[V] = E0
+    offsets_from_sorted(dev, dh.p, E0, Vl, L->roff.p, 0);  // roff[0..Vl], roff[Vl] = E0
   }
   if (P > 0) {
-    GG_CUDA(cudaMemcpy(L->roff.p + V, pstart.p, P * 8, cudaMemcpyDeviceToDevice));
+    GG_CUDA(cudaMemcpy(L->roff.p + Vl, pstart.p, P * 8, cudaMemcpyDeviceToDevice));
     L->owner.alloc(P);
     k_pair_owner<<<grid_for(P, 256, dev), 256>>>(keys.p, pstart.p, P, nvb, L->owner.p);
     GG_LAUNCH_CHECK();
   }
-  GG_CUDA(cudaMemcpy(L->roff.p + V + P, &E, 8, cudaMemcpyHostToDevice));
+  GG_CUDA(cudaMemcpy(L->roff.p + Vl + P, &E, 8, cudaMemcpyHostToDevice));
   // segment row ranges: cold pairs are sorted by segment; find boundaries by
   // binary search through the pair keys (K is small)
-  L->seg_row.assign(L->K + 1, V + P);
+  L->seg_row.assign(L->K + 1, Vl + P);
   L->seg_row[0] = 0;
-  if (L->K > 1) L->seg_row[1] = V;
+  if (L->K > 1) L->seg_row[1] = Vl;
   for (int64_t k = 2; k < L->K; ++k) {
     int64_t lo = 0, hi = P;
     while (lo < hi) {
@@ -270,7 +304,7 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
       int64_t e = dget(pstart.p + mid);
       if ((int64_t)(dget(keys.p + e) >> shift) < k) lo = mid + 1; else hi = mid;
     }
-    L->seg_row[k] = V + lo;
+    L->seg_row[k] = Vl + lo;
   }
   L->seg_edge.resize(L->K + 1);
   for (int64_t k = 0; k <= L->K; ++k) L->seg_edge[k] = dget(L->roff.p + L->seg_row[k]);
@@ -279,14 +313,14 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   return L;
 }
 
-// cached on the graph (one layout per (window, contrib width))
-static PrBlockLayout* layout_for(const Graph& gc, int64_t ns, int ct_bytes) {
+// cached on the graph (one layout per (window, contrib width, partition))
+static PrBlockLayout* layout_for(const Graph& gc, int64_t ns, int ct_bytes, PrPart part = PrPart()) {
   Graph& g = const_cast<Graph&>(gc);
   std::lock_guard<std::mutex> lk(g.mu);
   auto* cur = static_cast<PrBlockLayout*>(g.pr_block.get());
-  if (cur && cur->ns == ns && cur->ct_bytes == ct_bytes) return cur;
+  if (cur && cur->ns == ns && cur->ct_bytes == ct_bytes && cur->P == part.P && cur->r == part.r) return cur;
   g.pr_block.reset();  // free the previous layout before building another
-  auto L = build_layout(g, ns, ct_bytes);
+  auto L = build_layout(g, ns, ct_bytes, part);
   g.pr_block = L;
   return L.get();
 }
@@ -496,8 +530,8 @@ template <class CT>
 __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restrict__ outdeg,
                                                double* __restrict__ rank, CT* __restrict__ contrib_next,
                                                double* __restrict__ acc, double* scal, int64_t it,
-                                               double damping) {
-  const double n = (double)V;
+                                               double damping, int64_t nglob) {
+  const double n = (double)nglob;
   const double base = (1.0 - damping) / n + damping * scal[2 * it] / n;
   double l1 = 0, dm = 0;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -539,10 +573,10 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
 }
 
 template <class CT>
-static __global__ void __launch_bounds__(256) k_pr_vertex(int64_t V, const int32_t* outdeg, double* rank,
+static __global__ void __launch_bounds__(256) k_pr_vertex(int64_t V, int64_t nglob, const int32_t* outdeg, double* rank,
                                                           CT* contrib_next, double* acc, double* scal,
                                                           int64_t it, double damping) {
-  pr_vertex_pass<CT>(V, outdeg, rank, contrib_next, acc, scal, it, damping);
+  pr_vertex_pass<CT>(V, outdeg, rank, contrib_next, acc, scal, it, damping, nglob);
 }
 
 // Whole loop in one cooperative launch (kernel fusion on "s0").
@@ -563,13 +597,137 @@ static __global__ void __launch_bounds__(256) k_prb_fused(const int32_t* src, co
       pr_edges_seg<CT>(src, dst, seg_edge[s], seg_edge[s + 1], cur, acc, 1);
       grid.sync();
     }
-    pr_vertex_pass<CT>(V, outdeg, rank, nxt, acc, scal, it, damping);
+    pr_vertex_pass<CT>(V, outdeg, rank, nxt, acc, scal, it, damping, V);
     grid.sync();
     l1 = *((volatile double*)scal + 2 * it + 1);
     ++it;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *iters_out = it;
 }
+
+// ---------------------------------------------------------------------------
+// Host side.  One PrRank is one destination partition's state; a single-GPU
+// run is one PrRank with no exchange, a multi-GPU run one PrRank per process
+// with an NCCL exchange (dist.cu), and the virtual-rank test mode P PrRanks
+// on one device with a copy exchange.
+// ---------------------------------------------------------------------------
+struct HotCfg {
+  int32_t nhot = 0;
+  int per_sm = 1;
+  bool prefetch = true;
+  unsigned grid = 0, hot_grid = 0;
+};
+
+template <class CT>
+static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
+  // shared-memory hot-source cache for the hot segment: the top `nhot`
+  // sources (as many as fit next to the CTA).  GG_PR_HOT=0 disables it,
+  // GG_PR_HOT_THREADS picks 1024x1 (default) or 512x2 CTAs per SM,
+  // GG_PR_NHOT caps the cached count, GG_PR_PREFETCH=0 drops the register
+  // prefetch of the next edge step.
+  HotCfg h;
+  int smem_max = 0;
+  GG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const char* hot_env = getenv("GG_PR_HOT");
+  const bool hot_on = !(hot_env && atoi(hot_env) == 0);
+  const char* thr_env = getenv("GG_PR_HOT_THREADS");
+  h.per_sm = thr_env && atoi(thr_env) == 512 ? 2 : 1;
+  int smem_per_cta = h.per_sm == 2 ? (smem_max - 4096) / 2 : smem_max - 2048;
+  int64_t nhot64 = std::min<int64_t>(smem_per_cta / (int)sizeof(CT), L->ns);
+  if (const char* nh = getenv("GG_PR_NHOT")) nhot64 = std::min<int64_t>(nhot64, atoll(nh));
+  nhot64 &= ~int64_t(3);
+  h.nhot = hot_on && nhot64 >= 1024 ? (int32_t)nhot64 : 0;
+  if (h.nhot) {
+    const void* fn = h.per_sm == 2 ? (const void*)k_pr_edges_hot<CT, 512, 2> : (const void*)k_pr_edges_hot<CT, 1024, 1>;
+    GG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
+  }
+  const char* pf_env = getenv("GG_PR_PREFETCH");
+  h.prefetch = !(pf_env && atoi(pf_env) == 0);
+  h.grid = (unsigned)sm_count(dev) * 8;
+  h.hot_grid = (unsigned)sm_count(dev) * h.per_sm;
+  return h;
+}
+
+template <class CT>
+struct PrRank {
+  PrBlockLayout* L = nullptr;
+  HotCfg hc;
+  int dev = 0;
+  int64_t V = 0;
+  double *rank = nullptr, *acc = nullptr, *scal = nullptr, *outv = nullptr;
+  CT *c0 = nullptr, *c1 = nullptr;
+  int launches = 0;
+
+  // buffers: the layout's cached work buffers (rank/contrib full V, acc Vloc)
+  void bind(PrBlockLayout* lay, int device, int64_t iters_cap) {
+    L = lay;
+    dev = device;
+    V = L->V;
+    if (L->w_rank.n < (size_t)V) {
+      L->w_rank.alloc(V);
+      L->w_out.alloc(V);
+      L->w_c0.alloc(V * sizeof(CT));
+      L->w_c1.alloc(V * sizeof(CT));
+    }
+    if (L->w_acc.n < (size_t)std::max<int64_t>(L->vloc(), 1)) L->w_acc.alloc(std::max<int64_t>(L->vloc(), 1));
+    if (L->w_scal.n < (size_t)(2 * (iters_cap + 2))) L->w_scal.alloc(2 * (iters_cap + 2));
+    rank = L->w_rank.p;
+    acc = L->w_acc.p;
+    scal = L->w_scal.p;
+    outv = L->w_out.p;
+    c0 = reinterpret_cast<CT*>(L->w_c0.p);
+    c1 = reinterpret_cast<CT*>(L->w_c1.p);
+    hc = hot_cfg<CT>(dev, L);
+  }
+  // rank_0 = 1/n, contrib_0, dangling mass_0 over ALL vertices (identical on
+  // every rank, so no exchange precedes the first iteration)
+  void init(int64_t iters_cap, cudaStream_t st) {
+    GG_CUDA(cudaMemsetAsync(scal, 0, 2 * (iters_cap + 2) * sizeof(double), st));
+    GG_CUDA(cudaMemsetAsync(acc, 0, std::max<int64_t>(L->vloc(), 1) * sizeof(double), st));
+    k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank, c0, scal);
+    GG_LAUNCH_CHECK();
+    ++launches;
+  }
+  CT* cur(int64_t it) const { return (it & 1) ? c1 : c0; }
+  CT* nxt(int64_t it) const { return (it & 1) ? c0 : c1; }
+  // Alg. 2: segments in order, cold first, the hot one last
+  void edges(int64_t it, cudaStream_t st) {
+    const CT* c = cur(it);
+    for (int64_t k = 1; k <= L->K; ++k) {
+      const int64_t sg = k == L->K ? 0 : k;
+      const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
+      if (e1 <= e0) continue;
+      if (sg == 0 && hc.nhot > 0 && hc.per_sm == 2)
+        k_pr_edges_hot<CT, 512, 2><<<hc.hot_grid, 512, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, c,
+                                                                                  acc, hc.nhot);
+      else if (sg == 0 && hc.nhot > 0)
+        k_pr_edges_hot<CT, 1024, 1><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1,
+                                                                                    c, acc, hc.nhot);
+      else if (hc.prefetch)
+        k_pr_edges<CT, true><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+      else
+        k_pr_edges<CT, false><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+      ++launches;
+    }
+    GG_LAUNCH_CHECK();
+  }
+  // owned destinations [lo, hi): rank', L1 partial, next dangling partial,
+  // next contrib slice, acc reset
+  void vertex(int64_t it, double damping, cudaStream_t st) {
+    const int64_t lo = L->lo, n = L->vloc();
+    if (n > 0)
+      k_pr_vertex<CT><<<grid_for(n, 256, dev), 256, 0, st>>>(n, V, L->outdeg.p + lo, rank + lo, nxt(it) + lo, acc,
+                                                             scal, it, damping);
+    GG_LAUNCH_CHECK();
+    ++launches;
+  }
+  void unpermute(double* ranks_out, cudaStream_t st) {
+    k_unpermute<<<grid_for(V, 256, dev), 256, 0, st>>>(rank, L->newid.p, V, outv);
+    GG_LAUNCH_CHECK();
+    ++launches;
+    GG_CUDA(cudaMemcpyAsync(ranks_out, outv, V * 8, cudaMemcpyDefault, st));
+  }
+};
 
 template <class CT>
 int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int64_t max_iters,
@@ -580,80 +738,22 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   PrBlockLayout* L = layout_for(g, pr_block_window(g, sizeof(CT), s.blocking_size), sizeof(CT));
   const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
   std::lock_guard<std::mutex> wlk(L->w_mu);
-  if (L->w_rank.n < (size_t)V) {
-    L->w_rank.alloc(V);
-    L->w_acc.alloc(V);
-    L->w_out.alloc(V);
-    L->w_c0.alloc(V * sizeof(CT));
-    L->w_c1.alloc(V * sizeof(CT));
-  }
-  if (L->w_scal.n < (size_t)(2 * (iters_cap + 2))) L->w_scal.alloc(2 * (iters_cap + 2));
-  struct Ptr { double* p; };
-  struct CPtr { CT* p; };
-  Ptr rank{L->w_rank.p}, acc{L->w_acc.p}, scal{L->w_scal.p}, outv{L->w_out.p};
-  CPtr c0{reinterpret_cast<CT*>(L->w_c0.p)}, c1{reinterpret_cast<CT*>(L->w_c1.p)};
-  GG_CUDA(cudaMemsetAsync(scal.p, 0, 2 * (iters_cap + 2) * sizeof(double), st));
-  GG_CUDA(cudaMemsetAsync(acc.p, 0, V * sizeof(double), st));
-  k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank.p, c0.p, scal.p);
-  GG_LAUNCH_CHECK();
-  count_launch();
+  PrRank<CT> R;
+  R.bind(L, dev, iters_cap);
+  R.init(iters_cap, st);
   int64_t it = 0;
   if (!fusion) {
     double l1 = INFINITY;
-    const unsigned grid = (unsigned)sm_count(dev) * 8;
-    // shared-memory hot-source cache for the hot segment: the top `nhot`
-    // sources (as many as fit next to the CTA).  GG_PR_HOT=0 disables it,
-    // GG_PR_HOT_THREADS picks 1024x1 (default) or 512x2 CTAs per SM,
-    // GG_PR_NHOT caps the cached count.
-    int smem_max = 0;
-    GG_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const char* hot_env = getenv("GG_PR_HOT");
-    const bool hot_on = !(hot_env && atoi(hot_env) == 0);
-    const char* thr_env = getenv("GG_PR_HOT_THREADS");
-    const int hot_threads = thr_env && atoi(thr_env) == 512 ? 512 : 1024;
-    const int per_sm = hot_threads == 512 ? 2 : 1;
-    int smem_per_cta = smem_max - 2048;
-    if (per_sm == 2) smem_per_cta = (smem_max - 4096) / 2;
-    int64_t nhot64 = std::min<int64_t>(smem_per_cta / (int)sizeof(CT), L->ns);
-    if (const char* nh = getenv("GG_PR_NHOT")) nhot64 = std::min<int64_t>(nhot64, atoll(nh));
-    nhot64 &= ~int64_t(3);
-    int32_t nhot = hot_on && nhot64 >= 1024 ? (int32_t)nhot64 : 0;
-    const void* hot_fn = per_sm == 2 ? (const void*)k_pr_edges_hot<CT, 512, 2> : (const void*)k_pr_edges_hot<CT, 1024, 1>;
-    if (nhot)
-      GG_CUDA(cudaFuncSetAttribute(hot_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, nhot * (int)sizeof(CT)));
-    const unsigned hot_grid = (unsigned)sm_count(dev) * per_sm;
-    const char* pf_env = getenv("GG_PR_PREFETCH");  // register prefetch of the next edge step
-    const bool prefetch = !(pf_env && atoi(pf_env) == 0);
     while (!(it >= max_iters || l1 < tol)) {
-      const CT* cur = (it & 1) ? c1.p : c0.p;
-      CT* nxt = (it & 1) ? c0.p : c1.p;
       rt.edge_begin();
-      for (int64_t k = 1; k <= L->K; ++k) {  // Alg. 2: segments in order, cold first, hot last
-        const int64_t sg = k == L->K ? 0 : k;
-        const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
-        if (e1 <= e0) continue;
-        if (sg == 0 && nhot > 0 && per_sm == 2)
-          k_pr_edges_hot<CT, 512, 2><<<hot_grid, 512, nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, cur,
-                                                                             acc.p, nhot);
-        else if (sg == 0 && nhot > 0)
-          k_pr_edges_hot<CT, 1024, 1><<<hot_grid, 1024, nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, cur,
-                                                                               acc.p, nhot);
-        else if (prefetch)
-          k_pr_edges<CT, true><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
-        else
-          k_pr_edges<CT, false><<<grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, cur, acc.p);
-        count_launch();
-      }
+      R.edges(it, st);
       rt.edge_end();
-      k_pr_vertex<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(V, L->outdeg.p, rank.p, nxt, acc.p, scal.p, it,
-                                                             damping);
-      count_launch();
-      GG_LAUNCH_CHECK();
+      R.vertex(it, damping, st);
       rt.stats.dispatch_count += 1;
       rt.stats.direction_log.push_back(s.direction);
       ++it;
       if (tol > 0.0) {
-        GG_CUDA(cudaMemcpyAsync(&l1, scal.p + 2 * (it - 1) + 1, 8, cudaMemcpyDeviceToHost, st));
+        GG_CUDA(cudaMemcpyAsync(&l1, R.scal + 2 * (it - 1) + 1, 8, cudaMemcpyDeviceToHost, st));
         GG_CUDA(cudaStreamSynchronize(st));
       }
     }
@@ -667,28 +767,26 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
     int64_t K = L->K;
     int64_t Vv = V;
     const int32_t* od = L->outdeg.p;
-    double* rk = rank.p;
-    CT* p0 = c0.p;
-    CT* p1 = c1.p;
-    double* ac = acc.p;
-    double* sc = scal.p;
+    double* rk = R.rank;
+    CT* p0 = R.c0;
+    CT* p1 = R.c1;
+    double* ac = R.acc;
+    double* sc = R.scal;
     int64_t* ip = iters.p;
     void* args[] = {&sp, &dp, &se, &K, &Vv, &od, &rk, &p0, &p1, &ac, &sc, &max_iters, &tol, &damping, &ip};
     rt.edge_begin();
     GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_prb_fused<CT>, blocks, 256, args, 0, st));
     rt.edge_end();
-    count_launch();
+    ++R.launches;
     it = dget(iters.p);
     rt.stats.dispatch_count += 1;
     for (int64_t k = 0; k < it; ++k) rt.stats.direction_log.push_back(s.direction);
   }
   rt.stats.rounds += it;
   rt.stats.edges_traversed += it * g.E;
-  k_unpermute<<<grid_for(V, 256, dev), 256, 0, st>>>(rank.p, L->newid.p, V, outv.p);
-  GG_LAUNCH_CHECK();
-  count_launch();
-  GG_CUDA(cudaMemcpyAsync(ranks_out, outv.p, V * 8, cudaMemcpyDefault, st));
+  R.unpermute(ranks_out, st);
   GG_CUDA(cudaStreamSynchronize(st));
+  count_launch(R.launches);
   return it;
 }
 
@@ -696,5 +794,137 @@ template int64_t pagerank_blocked<double>(const Graph&, const gg_schedule&, bool
                                           double, double*, Runtime&);
 template int64_t pagerank_blocked<float>(const Graph&, const gg_schedule&, bool, int64_t, double,
                                          double, double*, Runtime&);
+
+// ---------------------------------------------------------------------------
+// Partitioned (multi-rank) run.  Per iteration: local edge phase over the
+// owned destinations' in-edges, vertex pass over the owned slice, then the
+// exchange: all-reduce of (L1 this iteration, dangling mass next iteration)
+// -- adjacent doubles -- and all-gather of the owned next-contrib slices.
+// ---------------------------------------------------------------------------
+template <class CT>
+int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, int64_t max_iters, double tol,
+                               double damping, int32_t direction_log, cudaStream_t st, Runtime& rt) {
+  const PrBlockLayout* L0 = ranks[0]->L;
+  int64_t it = 0;
+  double l1 = INFINITY;
+  std::vector<double*> sc(ranks.size());
+  std::vector<void*> nx(ranks.size());
+  while (!(it >= max_iters || l1 < tol)) {
+    rt.edge_begin();
+    for (auto* R : ranks) R->edges(it, st);
+    rt.edge_end();
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      ranks[i]->vertex(it, damping, st);
+      sc[i] = ranks[i]->scal + 2 * it + 1;
+      nx[i] = ranks[i]->nxt(it);
+    }
+    ex.allreduce2(sc, st);
+    ex.allgather(nx, sizeof(CT), L0->bounds, st);
+    rt.stats.dispatch_count += 1;
+    rt.stats.direction_log.push_back(direction_log);
+    ++it;
+    if (tol > 0.0) {
+      GG_CUDA(cudaMemcpyAsync(&l1, ranks[0]->scal + 2 * (it - 1) + 1, 8, cudaMemcpyDeviceToHost, st));
+      GG_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  // every rank's owned rank slice to all ranks
+  std::vector<void*> rk(ranks.size());
+  for (size_t i = 0; i < ranks.size(); ++i) rk[i] = ranks[i]->rank;
+  ex.allgather(rk, sizeof(double), L0->bounds, st);
+  rt.stats.rounds += it;
+  return it;
+}
+
+// Virtual ranks on one device (test mode for the multi-GPU path): P
+// partitions, each with its own layout and buffers; the exchange copies.
+struct CopyExchange : PrExchange {
+  void allreduce2(std::vector<double*>& d, cudaStream_t st) override {
+    std::vector<double> h(2 * d.size());
+    for (size_t i = 0; i < d.size(); ++i)
+      GG_CUDA(cudaMemcpyAsync(&h[2 * i], d[i], 16, cudaMemcpyDeviceToHost, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+    double s[2] = {0, 0};
+    for (size_t i = 0; i < d.size(); ++i) {  // rank order, as a ring reduce would
+      s[0] += h[2 * i];
+      s[1] += h[2 * i + 1];
+    }
+    for (size_t i = 0; i < d.size(); ++i) GG_CUDA(cudaMemcpyAsync(d[i], s, 16, cudaMemcpyHostToDevice, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+  }
+  void allgather(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                 cudaStream_t st) override {
+    for (size_t r = 0; r < bufs.size(); ++r) {
+      const size_t off = (size_t)bounds[r] * elt, len = (size_t)(bounds[r + 1] - bounds[r]) * elt;
+      for (size_t q = 0; q < bufs.size(); ++q)
+        if (q != r && len)
+          GG_CUDA(cudaMemcpyAsync((char*)bufs[q] + off, (char*)bufs[r] + off, len, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+};
+
+template <class CT>
+int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int nparts, int64_t max_iters, double tol,
+                                 double damping, double* ranks_out, Runtime& rt) {
+  if (nparts < 1) fail(GG_ERR_VALUE, "nparts must be >= 1");
+  const int64_t ns = pr_block_window(g, sizeof(CT), s.blocking_size);
+  const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
+  std::vector<std::shared_ptr<PrBlockLayout>> lays;
+  std::vector<PrRank<CT>> rs(nparts);
+  std::vector<PrRank<CT>*> rp;
+  int64_t local_edges = 0;
+  for (int r = 0; r < nparts; ++r) {
+    lays.push_back(build_layout(g, ns, sizeof(CT), PrPart{nparts, r}));
+    rs[r].bind(lays.back().get(), g.dev, iters_cap);
+    rs[r].init(iters_cap, rt.stream);
+    rp.push_back(&rs[r]);
+    local_edges += lays.back()->E;
+  }
+  if (local_edges != g.E) fail(GG_ERR_ENGINE, "partition lost edges");
+  CopyExchange ex;
+  int64_t it = pagerank_blocked_ranks<CT>(rp, ex, max_iters, tol, damping, s.direction, rt.stream, rt);
+  rt.stats.edges_traversed += it * g.E;
+  rs[0].unpermute(ranks_out, rt.stream);
+  GG_CUDA(cudaStreamSynchronize(rt.stream));
+  int launches = 0;
+  for (auto& R : rs) launches += R.launches;
+  count_launch(launches);
+  return it;
+}
+template int64_t pagerank_blocked_virtual<double>(const Graph&, const gg_schedule&, int, int64_t, double, double,
+                                                  double*, Runtime&);
+template int64_t pagerank_blocked_virtual<float>(const Graph&, const gg_schedule&, int, int64_t, double, double,
+                                                 double*, Runtime&);
+
+// One rank of a multi-process run (dist.cu supplies the NCCL exchange).
+template <class CT>
+int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r, PrExchange& ex,
+                              int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
+                              int64_t* local_edges) {
+  const int64_t ns = pr_block_window(g, sizeof(CT), s.blocking_size);
+  PrBlockLayout* L = layout_for(g, ns, sizeof(CT), PrPart{P, r});
+  const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
+  std::lock_guard<std::mutex> wlk(L->w_mu);
+  PrRank<CT> R;
+  R.bind(L, g.dev, iters_cap);
+  R.init(iters_cap, rt.stream);
+  std::vector<PrRank<CT>*> rp{&R};
+  int64_t it = pagerank_blocked_ranks<CT>(rp, ex, max_iters, tol, damping, s.direction, rt.stream, rt);
+  rt.stats.edges_traversed += it * L->E;
+  if (local_edges) *local_edges = L->E;
+  R.unpermute(ranks_out, rt.stream);
+  GG_CUDA(cudaStreamSynchronize(rt.stream));
+  count_launch(R.launches);
+  return it;
+}
+template int64_t pagerank_blocked_rank<double>(const Graph&, const gg_schedule&, int, int, PrExchange&, int64_t,
+                                               double, double, double*, Runtime&, int64_t*);
+template int64_t pagerank_blocked_rank<float>(const Graph&, const gg_schedule&, int, int, PrExchange&, int64_t,
+                                              double, double, double*, Runtime&, int64_t*);
+
+double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r) {
+  PrBlockLayout* L = layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes, PrPart{P, r});
+  return L->prep_ms;
+}
 
 }  // namespace gg

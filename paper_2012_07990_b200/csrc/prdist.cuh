@@ -1,0 +1,32 @@
+// prdist.cuh — the exchange step of a destination-partitioned PageRank run
+// and the partitioned EdgeBlocking entry points (prblock.cu).
+#pragma once
+#include "engine.cuh"
+#include <vector>
+
+namespace gg {
+
+// After each vertex pass every rank holds (a) two f64 partial sums -- the L1
+// of this iteration and the dangling mass of the next, adjacent in memory --
+// and (b) its owned slice [bounds[r], bounds[r+1]) of the next contribution
+// vector.  The exchange sums (a) over ranks in place and gives (b) to every
+// rank.  NCCL implements it across processes (dist.cu); CopyExchange across
+// virtual ranks on one device (prblock.cu, test mode).  `d`/`bufs` hold one
+// pointer per rank this process drives.
+struct PrExchange {
+  virtual ~PrExchange() {}
+  virtual void allreduce2(std::vector<double*>& d, cudaStream_t st) = 0;
+  virtual void allgather(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                         cudaStream_t st) = 0;
+};
+
+template <class CT>
+int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r, PrExchange& ex,
+                              int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
+                              int64_t* local_edges);
+template <class CT>
+int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int nparts, int64_t max_iters, double tol,
+                                 double damping, double* ranks_out, Runtime& rt);
+double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r);
+
+}  // namespace gg

@@ -59,9 +59,49 @@ class Comm:
             self._h = None
 
 
-def pagerank_dist(comm, g, max_iters=100, tolerance=1e-9, damping=0.85, out=None):
+def _binding(program):
+    from .algos import _plan
+    from .engine import binding_pod
+    plan = _plan(program, "pagerank")
+    return binding_pod(plan.apply_schedule)
+
+
+def pagerank_dist(comm, g, max_iters=100, tolerance=1e-9, damping=0.85, out=None,
+                  program=None, contrib_fp32=False):
+    """This rank's share of a partitioned PageRank; returns the full rank
+    vector (gathered on every rank) and this rank's RunStats.  With an
+    EDGE_ONLY + BLOCKED program the EdgeBlocking layout of the owned
+    destinations runs; otherwise the PULL gather (no program = PULL)."""
     ranks = out if out is not None else np.empty(g.num_vertices, np.float64)
     st = _lib.new_stats()
-    _lib.call("gg_pagerank_dist", comm._h, g.handle, int(max_iters), float(tolerance),
-              float(damping), _lib.ptr(ranks), C.byref(st))
+    if program is None:
+        _lib.call("gg_pagerank_dist", comm._h, g.handle, int(max_iters), float(tolerance),
+                  float(damping), _lib.ptr(ranks), C.byref(st))
+    else:
+        pod = _binding(program)
+        _lib.call("gg_pagerank_dist_ex", comm._h, g.handle, C.byref(pod),
+                  1 if contrib_fp32 else 0, int(max_iters), float(tolerance), float(damping),
+                  _lib.ptr(ranks), C.byref(st))
+    return ranks, RunStats.from_pod(st)
+
+
+def prepare_dist(nranks, rank, g, program, contrib_fp32=False):
+    """Build this rank's layout ahead of the timed runs; returns prep ms."""
+    pod = _binding(program)
+    ms = C.c_double()
+    _lib.call("gg_pagerank_dist_prepare", int(nranks), int(rank), g.handle, C.byref(pod),
+              1 if contrib_fp32 else 0, C.byref(ms))
+    return ms.value
+
+
+def pagerank_virtual(g, nparts, program, max_iters=100, tolerance=1e-9, damping=0.85,
+                     out=None, contrib_fp32=False):
+    """The partitioned EdgeBlocking run with `nparts` virtual ranks on one
+    device (copy exchange) -- the test mode of the multi-GPU path."""
+    ranks = out if out is not None else np.empty(g.num_vertices, np.float64)
+    st = _lib.new_stats()
+    pod = _binding(program)
+    _lib.call("gg_pagerank_virtual", g.handle, int(nparts), C.byref(pod),
+              1 if contrib_fp32 else 0, int(max_iters), float(tolerance), float(damping),
+              _lib.ptr(ranks), C.byref(st))
     return ranks, RunStats.from_pod(st)

@@ -22,3 +22,54 @@ def test_pagerank_dist_single_rank_matches_oracle():
     assert np.max(np.abs(ranks - want) / want) < 1e-6
     assert st.rounds == 20
     comm.close()
+
+
+def _eb_program(gg, blocking_size=None):
+    return gg.ScheduleProgram({"s0:s1": gg.Schedule(load_balance="EDGE_ONLY", blocking=True,
+                                                    blocking_size=blocking_size)})
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("nparts", [1, 2, 3, 4, 8])
+def test_pagerank_virtual_ranks_match_oracle(nparts, fp32):
+    """The partitioned EdgeBlocking run (per-rank layouts over owned
+    destinations + exchange) with virtual ranks on one device."""
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.dist import pagerank_virtual
+    V, s, d = gen.rmat(12, 16, seed=5)
+    g = gg.Graph.from_coo(V, s, d)
+    want, _ = oracle.pagerank(V, s, d, 20, 0.0)
+    for bs in (None, 300):  # default window (hot segment only) and many cold segments
+        ranks, st = pagerank_virtual(g, nparts, _eb_program(gg, bs), max_iters=20, tolerance=0.0,
+                                     contrib_fp32=fp32)
+        assert np.max(np.abs(ranks - want) / want) < 1e-6, (nparts, bs)
+        assert st.rounds == 20
+        assert st.edges_traversed == 20 * len(s)
+
+
+def test_pagerank_virtual_ranks_tolerance_and_tiny_partitions():
+    """More ranks than 32-vertex partition blocks (empty ranks) and the L1
+    stop test summed over ranks."""
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.dist import pagerank_virtual
+    V, s, d = gen.rmat(6, 4, seed=9)
+    g = gg.Graph.from_coo(V, s, d)
+    want, it = oracle.pagerank(V, s, d, 100, 1e-9)
+    ranks, st = pagerank_virtual(g, 8, _eb_program(gg), max_iters=100, tolerance=1e-9)
+    assert np.max(np.abs(ranks - want) / want) < 1e-6
+    assert st.rounds == it
+
+
+def test_pagerank_dist_ex_single_rank_edgeblocking():
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.dist import Comm, pagerank_dist, prepare_dist
+    V, s, d = gen.rmat(12, 16, seed=5)
+    g = gg.Graph.from_coo(V, s, d)
+    prog = _eb_program(gg)
+    assert prepare_dist(1, 0, g, prog) >= 0.0
+    comm = Comm.create(0, 1, 0)
+    ranks, st = pagerank_dist(comm, g, max_iters=20, tolerance=0.0, program=prog)
+    want, _ = oracle.pagerank(V, s, d, 20, 0.0)
+    assert np.max(np.abs(ranks - want) / want) < 1e-6
+    assert st.rounds == 20
+    comm.close()
