@@ -133,7 +133,7 @@ def sssp_c3(gg, args, peak):
         off = np.asarray(g.out_offsets, dtype=np.int64)
         nbr = np.asarray(g.out_neighbors, dtype=np.int32)
         w = np.asarray(g.out_weights, dtype=np.uint32)
-        want = oracle.sssp_delta(V, off, nbr, w, 0, best)
+        want, _ = oracle.sssp_delta(V, off, nbr, w, 0, best)
         prog = gg.ScheduleProgram({"s0:s1": gg.Schedule(direction="PUSH", load_balance=args.lb,
                                                         delta=best),
                                    "s0": gg.Schedule(kernel_fusion=True)})
@@ -192,7 +192,7 @@ def cc_bc_c4(gg, args, peak):
         bc_res[lb]["gteps"] = 2.0 * sum(m_c) / (bc_res[lb]["ms"] * 1e-3) / 1e9
     if args.check:
         import oracle
-        want = oracle.cc(V, np.asarray(g.coo_src), np.asarray(g.coo_dst))
+        want, _ = oracle.cc(V, np.asarray(g.coo_src), np.asarray(g.coo_dst))
         assert np.array_equal(lab, want)
     head = lbs[0]
     ms = cc_res[head]["ms"]

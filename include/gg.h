@@ -252,6 +252,17 @@ int gg_pagerank_dist_ex(gg_comm* c, const gg_graph* g, const gg_binding* binding
 /* Build (and cache) rank `rank` of `nranks`'s layout without running. */
 int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g,
                              const gg_binding* binding, int32_t fp32_contrib, double* prep_ms);
+/* Direction-optimizing BFS, 1-D vertex partition (32-aligned, balanced by
+ * out-degree), bitmap frontier exchange: top-down levels all-reduce(max)
+ * parent candidates, bottom-up levels all-gather the owned next-frontier
+ * words; PULL iff |frontier| > threshold*V (engine.hybrid_apply,
+ * engine.py:622-636; algos.bfs, algos.py:101-135).  parents: V, gathered on
+ * every rank; a legal BFS tree with the single-GPU depths. */
+int gg_bfs_dist(gg_comm* c, const gg_graph* g, int64_t source, double threshold,
+                int32_t* parents, gg_stats* stats);
+/* The same with `nparts` virtual ranks on the graph's one device (test mode). */
+int gg_bfs_virtual(const gg_graph* g, int32_t nparts, int64_t source, double threshold,
+                   int32_t* parents, gg_stats* stats);
 /* Test mode of the partitioned run: `nparts` virtual ranks on the graph's
  * one device, each with its own layout and buffers, exchanging by copies in
  * the same order as the NCCL exchange.  EDGE_ONLY + BLOCKED only. */

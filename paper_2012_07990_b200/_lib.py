@@ -125,6 +125,8 @@ SIGNATURES = {
                                   C.POINTER(GGStats)]),
     "gg_pagerank_dist_prepare": (I32, [I32, I32, VP, C.POINTER(GGBinding), I32,
                                        C.POINTER(F64)]),
+    "gg_bfs_dist": (I32, [VP, VP, I64, F64, VP, C.POINTER(GGStats)]),
+    "gg_bfs_virtual": (I32, [VP, I32, I64, F64, VP, C.POINTER(GGStats)]),
     "gg_pagerank_virtual": (I32, [VP, I32, C.POINTER(GGBinding), I32, I64, F64, F64, VP,
                                   C.POINTER(GGStats)]),
 }

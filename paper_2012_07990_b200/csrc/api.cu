@@ -46,6 +46,7 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
 int64_t pagerank_dist_run(gg_comm* c, const Graph& g, int64_t max_iters, double tol, double damping,
                           double* ranks_out, Runtime& rt);
 double pr_block_prep_ms(const Graph& g, int64_t blocking_size, int ct_bytes);
+int64_t bfs_dist_run(gg_comm* c, const Graph& g, int64_t source, double theta, int32_t* parents_out, Runtime& rt);
 int64_t pagerank_dist_blocked(gg_comm* c, const Graph& g, const gg_schedule& s, bool fp32, int64_t max_iters,
                               double tol, double damping, double* ranks_out, Runtime& rt);
 inline void pr_block_prep(const Graph& g, int64_t blocking_size, int ct_bytes) {
@@ -579,6 +580,35 @@ int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g, co
   }
   GG_CUDA(cudaDeviceSynchronize());
   if (prep_ms) *prep_ms = now_ms() - t0;
+  GG_API_END
+}
+
+int gg_bfs_dist(gg_comm* c, const gg_graph* g, int64_t source, double threshold, int32_t* parents,
+                gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(c);
+  NEED(g);
+  NEED(parents);
+  if (!(threshold > 0.0 && threshold < 1.0)) fail(GG_ERR_SCHEDULE, "threshold must lie in (0, 1)");
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), nullptr);
+  CallTimer t(g->g->dev);
+  bfs_dist_run(c, *g->g, source, threshold, parents, rt);
+  t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_bfs_virtual(const gg_graph* g, int32_t nparts, int64_t source, double threshold, int32_t* parents,
+                   gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(parents);
+  if (!(threshold > 0.0 && threshold < 1.0)) fail(GG_ERR_SCHEDULE, "threshold must lie in (0, 1)");
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), nullptr);
+  CallTimer t(g->g->dev);
+  bfs_virtual(*g->g, nparts, source, threshold, parents, rt);
+  t.finish(g->g->dev, rt, stats);
   GG_API_END
 }
 

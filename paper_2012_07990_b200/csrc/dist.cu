@@ -168,6 +168,30 @@ struct NcclExchange : PrExchange {
   }
 };
 
+struct NcclBfsExchange : BfsExchange {
+  gg_comm* c;
+  explicit NcclBfsExchange(gg_comm* cc) : c(cc) {}
+  void allreduce_max_i32(std::vector<int32_t*>& bufs, int64_t n, cudaStream_t st) override {
+    GG_NCCL(nccl().AllReduce(bufs[0], bufs[0], (size_t)n, ncclInt32, ncclMax, c->comm, st));
+  }
+  void allgather_bytes(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                       cudaStream_t st) override {
+    NcclApi& api = nccl();
+    GG_NCCL(api.GroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+      const size_t cnt = (size_t)(bounds[r + 1] - bounds[r]) * elt;
+      char* p = (char*)bufs[0] + (size_t)bounds[r] * elt;
+      if (cnt) GG_NCCL(api.Broadcast(p, p, cnt, ncclUint8, r, c->comm, st));
+    }
+    GG_NCCL(api.GroupEnd());
+  }
+};
+
+int64_t bfs_dist_run(gg_comm* c, const Graph& g, int64_t source, double theta, int32_t* parents_out, Runtime& rt) {
+  NcclBfsExchange ex(c);
+  return bfs_rank(g, c->nranks, c->rank, ex, source, theta, parents_out, rt);
+}
+
 int64_t pagerank_dist_blocked(gg_comm* c, const Graph& g, const gg_schedule& s, bool fp32, int64_t max_iters,
                               double tol, double damping, double* ranks_out, Runtime& rt) {
   NcclExchange ex(c);

@@ -20,6 +20,19 @@ struct PrExchange {
                          cudaStream_t st) = 0;
 };
 
+// Exchange of the partitioned BFS (bfsdist.cu): an element-wise max of an
+// int32 array (top-down parent candidates) and an all-gather of owned slices
+// (bottom-up next-frontier words, final parents).
+struct BfsExchange {
+  virtual ~BfsExchange() {}
+  virtual void allreduce_max_i32(std::vector<int32_t*>& bufs, int64_t n, cudaStream_t st) = 0;
+  virtual void allgather_bytes(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                               cudaStream_t st) = 0;
+};
+int64_t bfs_virtual(const Graph& g, int nparts, int64_t source, double theta, int32_t* parents_out, Runtime& rt);
+int64_t bfs_rank(const Graph& g, int P, int r, BfsExchange& ex, int64_t source, double theta, int32_t* parents_out,
+                 Runtime& rt);
+
 template <class CT>
 int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r, PrExchange& ex,
                               int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,

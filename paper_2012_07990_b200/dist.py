@@ -105,3 +105,26 @@ def pagerank_virtual(g, nparts, program, max_iters=100, tolerance=1e-9, damping=
               1 if contrib_fp32 else 0, int(max_iters), float(tolerance), float(damping),
               _lib.ptr(ranks), C.byref(st))
     return ranks, RunStats.from_pod(st)
+
+
+def bfs_dist(comm, g, source, threshold=0.05, out=None):
+    """This rank's share of the partitioned direction-optimizing BFS; returns
+    the full parent array (gathered on every rank) and this rank's RunStats."""
+    if not 0 <= source < g.num_vertices:
+        raise ValueError("invalid source %d for graph with %d vertices" % (source, g.num_vertices))
+    parents = out if out is not None else np.empty(g.num_vertices, np.int32)
+    st = _lib.new_stats()
+    _lib.call("gg_bfs_dist", comm._h, g.handle, int(source), float(threshold), _lib.ptr(parents),
+              C.byref(st))
+    return parents, RunStats.from_pod(st)
+
+
+def bfs_virtual(g, nparts, source, threshold=0.05, out=None):
+    """The partitioned BFS with `nparts` virtual ranks on one device (test mode)."""
+    if not 0 <= source < g.num_vertices:
+        raise ValueError("invalid source %d for graph with %d vertices" % (source, g.num_vertices))
+    parents = out if out is not None else np.empty(g.num_vertices, np.int32)
+    st = _lib.new_stats()
+    _lib.call("gg_bfs_virtual", g.handle, int(nparts), int(source), float(threshold),
+              _lib.ptr(parents), C.byref(st))
+    return parents, RunStats.from_pod(st)

@@ -73,3 +73,48 @@ def test_pagerank_dist_ex_single_rank_edgeblocking():
     assert np.max(np.abs(ranks - want) / want) < 1e-6
     assert st.rounds == 20
     comm.close()
+
+
+def _levels_and_tree(gg, g, parents, source, off, nbr):
+    V = g.num_vertices
+    want = oracle.bfs_levels(V, off, nbr, source).tolist()
+    assert gg.bfs_levels(parents) == want
+    assert parents[source] == source
+    arcs = set(zip(g.coo_src.tolist(), g.coo_dst.tolist()))
+    for v, p in enumerate(parents.tolist()):
+        if v != source and p != -1:
+            assert (p, v) in arcs
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+@pytest.mark.parametrize("theta", [1e-9, 0.05, 0.999999])
+def test_bfs_virtual_ranks_levels_and_tree(nparts, theta):
+    """Partitioned direction-optimizing BFS with virtual ranks: always-pull,
+    hybrid and always-push thresholds; depths bit-exact vs the oracle,
+    parents a legal BFS tree."""
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.dist import bfs_virtual
+    g = gg.generate_rmat(11, 8, seed=3, symmetrize=True)
+    V = g.num_vertices
+    off, nbr, _ = oracle.csr(V, g.coo_src, g.coo_dst)
+    deg = np.diff(off)
+    for source in [int(np.argmax(deg)), int(np.flatnonzero(deg == 1)[0]), int(np.flatnonzero(deg == 0)[0])]:
+        parents, st = bfs_virtual(g, nparts, source, theta)
+        _levels_and_tree(gg, g, parents, source, off, nbr)
+        if theta == 1e-9:
+            assert set(st.direction_log) <= {1}
+        if theta == 0.999999:
+            assert set(st.direction_log) == {0}
+
+
+def test_bfs_dist_single_rank_matches_oracle():
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.dist import Comm, bfs_dist
+    g = gg.generate_rmat(11, 8, seed=3, symmetrize=True)
+    V = g.num_vertices
+    off, nbr, _ = oracle.csr(V, g.coo_src, g.coo_dst)
+    comm = Comm.create(0, 1, 0)
+    src = int(np.argmax(np.diff(off)))
+    parents, st = bfs_dist(comm, g, src, 0.05)
+    _levels_and_tree(gg, g, parents, src, off, nbr)
+    comm.close()
