@@ -107,7 +107,7 @@ def sssp_c3(gg, args, peak):
     g = gg.generate_grid(side, seed=4, weights=True)
     gen_s = time.perf_counter() - t0
     V, A = g.num_vertices, g.num_edges
-    deltas = [args.delta] if args.delta else [64, 256, 1024, 2048, 4096, 8192]
+    deltas = [args.delta] if args.delta else [1024, 4096, 8192, 16384, 32768, 65536]
     import torch
     dist = torch.empty(V, dtype=torch.int64, device="cuda")
     sweep = {}

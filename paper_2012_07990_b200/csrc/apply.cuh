@@ -11,6 +11,8 @@ void strict_spans(Runtime* rt, int64_t nspans);
 void clear_marks(Runtime* rt, Frontier* out, const OutBuilder& ob);
 Frontier* converted_view(Runtime* rt, Frontier* in, int repr);
 void twc_queues(Runtime* rt, TwcQueues* q);
+// ETWC huge-range queue (capacity E / kEtwcHuge + 1), count zeroed on the stream
+void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n);
 OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out);
 void dense_size_on_device(Frontier* f, cudaStream_t s);
 
@@ -33,9 +35,13 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
     case GG_LB_CM:
       k_push_cm<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
       break;
-    case GG_LB_ETWC:
+    case GG_LB_ETWC: {
+      etwc_huge(rt, &a.huge, &a.huge_n);
       k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
+      k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+      count_launch();
       break;
+    }
     case GG_LB_STRICT: {
       const int64_t n = n_host >= 0 ? n_host : g->V;
       strict_prefix(rt, in, n);

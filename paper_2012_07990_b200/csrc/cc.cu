@@ -27,7 +27,7 @@ __global__ void k_pointer_jump(int32_t* label, int64_t V, int* moved) {
       any = 1;
     }
   }
-  if (__any_sync(0xffffffffu, any) && lane_id() == 0) *moved = 1;
+  if (__any_sync(0xffffffffu, any) && lane_id() == 0 && !*((volatile int*)moved)) *moved = 1;
 }
 
 // first member (minimum id) of every label class, then relabel

@@ -322,10 +322,25 @@ void check_binding(const gg_binding& b) {
 // ---------------------------------------------------------------------------
 // Dispatch
 // ---------------------------------------------------------------------------
+void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n) {
+  const int64_t cap = rt->g->E / kEtwcHuge + 1;
+  if (rt->etwc_q.n < (size_t)cap) rt->etwc_q.alloc(cap);
+  if (!rt->etwc_n.p) rt->etwc_n.alloc(1);
+  GG_CUDA(cudaMemsetAsync(rt->etwc_n.p, 0, sizeof(unsigned long long), rt->stream));
+  *q = rt->etwc_q.p;
+  *n = rt->etwc_n.p;
+}
+
 int max_coop_blocks(const void* fn, int block, int dev, size_t smem) {
   int per_sm = 0;
   GG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
   if (per_sm < 1) fail(GG_ERR_CUDA, "kernel cannot be co-resident");
+  // grid-barrier cost grows with the CTA count; GG_COOP_PER_SM caps the
+  // resident CTAs per SM of cooperative (fused-loop) launches
+  if (const char* e = getenv("GG_COOP_PER_SM")) {
+    int cap = atoi(e);
+    if (cap >= 1 && cap < per_sm) per_sm = cap;
+  }
   return per_sm * sm_count(dev);
 }
 

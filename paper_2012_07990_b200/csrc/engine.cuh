@@ -55,6 +55,8 @@ struct Runtime {
   // scratch
   DevBuf<int32_t> twc_q;               // 3 * V
   DevBuf<unsigned long long> twc_cnt;  // 3
+  DevBuf<EtwcEntry> etwc_q;            // ETWC huge CTA-stage ranges
+  DevBuf<unsigned long long> etwc_n;
   DevBuf<int64_t> prefix;              // STRICT push prefix (V+1)
   DevBuf<int64_t> spans;               // STRICT pull spans
   int64_t spans_n = -1;

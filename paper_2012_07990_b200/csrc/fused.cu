@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) k_cc_fused(CcFusedArgs a) {
         int32_t l = a.label[v], ll = a.label[l];
         if (ll != l) { a.label[v] = ll; any = 1; }
       }
-      if (__any_sync(0xffffffffu, any) && lane_id() == 0) atomicOr(a.flags + 1, 1);
+      if (__any_sync(0xffffffffu, any) && lane_id() == 0 && !*((volatile int*)a.flags + 1)) atomicOr(a.flags + 1, 1);
       grid.sync();
       const int moved = *((volatile int*)a.flags + 1);
       grid.sync();  // every thread has read the flag before thread 0 resets it

@@ -21,6 +21,8 @@ struct FusedScratch {
   const int64_t* seg_end;  // EdgeBlocking segments (EDGE_ONLY + BLOCKED)
   int64_t nseg;
   CooView blocked;
+  EtwcEntry* etwc_q;             // ETWC huge CTA-stage ranges (grid pass)
+  unsigned long long* etwc_n;    // kept 0 between phases
 };
 
 // Grid-wide exclusive prefix of active out-degrees (STRICT push in a fused
@@ -98,7 +100,17 @@ __device__ __forceinline__ void fused_edge_phase(const gg_schedule& s, const Csr
       case GG_LB_VERTEX_BASED: b_push_vb<Op>(a); break;
       case GG_LB_WM: b_push_wm<Op>(a); break;
       case GG_LB_CM: b_push_cm<Op>(a); break;
-      case GG_LB_ETWC: b_push_etwc<Op>(a, cta); break;
+      case GG_LB_ETWC:
+        a.huge = sc.etwc_q;
+        a.huge_n = sc.etwc_n;
+        b_push_etwc<Op>(a, cta);
+        if (a.huge) {
+          grid.sync();
+          b_push_huge<Op>(a);
+          grid.sync();
+          if (tid == 0) *sc.etwc_n = 0;  // next append is behind the caller's barrier
+        }
+        break;
       case GG_LB_STRICT: {
         const int64_t n = active_count(in, out_csr.V);
         grid_degree_prefix(in, out_csr.off, n, sc.prefix, sc.block_sums, grid);
@@ -149,6 +161,7 @@ struct FusedHost {
     for (int k = 0; k < nsched; ++k) {
       const gg_schedule& s = *scheds[k];
       if (s.load_balance == GG_LB_TWC) twc_queues(&rt, &sc.twc);
+      if (s.load_balance == GG_LB_ETWC && s.direction == GG_PUSH) etwc_huge(&rt, &sc.etwc_q, &sc.etwc_n);
       if (s.load_balance == GG_LB_STRICT && s.direction == GG_PUSH) {
         prefix.alloc(g.V + 2);
         block_sums.alloc(coop_blocks + 1);

@@ -116,7 +116,9 @@ struct OpHook {
     int32_t la = *((volatile int32_t*)label + u), lb = *((volatile int32_t*)label + v);
     if (la == lb) return;
     int32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
-    if (atomicMin(label + hi, lo) > lo) *changed = 1;
+    // read before write: one hot flag line, written once per round instead of
+    // once per successful hook (which serialises at its L2 slice)
+    if (atomicMin(label + hi, lo) > lo && !*((volatile int*)changed)) *changed = 1;
   }
   __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
     hook(u, v);

@@ -157,6 +157,7 @@ __device__ __forceinline__ int upper_idx(F key, int n, int64_t x) {
 // PUSH (engine.py:463-503): per active source, scan out-edges, filter dst,
 // udf with atomic helpers.
 // ===========================================================================
+struct EtwcEntry;
 template <class Op>
 struct PushArgs {
   CsrView g;
@@ -165,6 +166,10 @@ struct PushArgs {
   OutBuilder out;
   int use_filter;
   unsigned long long* scanned;
+  // ETWC: CTA-stage ranges of at least kEtwcHuge edges go to this global
+  // queue and are processed by the whole grid afterwards (null: in-CTA)
+  EtwcEntry* huge = nullptr;
+  unsigned long long* huge_n = nullptr;
 };
 
 template <class Op>
@@ -426,6 +431,45 @@ struct EtwcEntry {
   int32_t u;
   __device__ __forceinline__ int64_t hi() const { return lo + len; }
 };
+// A single CTA walking a hub's whole CTA-stage range serialises on the hub
+// (RMAT/Kronecker hubs have 10^5-10^6 arcs, several can land in one CTA's
+// slice of the active list): such ranges are handed to the whole grid.
+constexpr int64_t kEtwcHuge = 16384;
+
+// Cooperative range walk with 4 independent arcs in flight per thread.
+template <class Op>
+__device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_t u, int64_t lo, int64_t hi,
+                                                   int64_t first, int64_t stride) {
+  int64_t e = lo + first;
+  for (; e + 3 * stride < hi; e += 4 * stride) {
+    int32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(a.g.nbr + e + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (a.use_filter && !a.op.filter(v[k])) continue;
+      uint32_t w = a.g.w ? __ldg(a.g.w + e + k * stride) : 0u;
+      a.op.push(u, v[k], w, a.out);
+    }
+  }
+  for (; e < hi; e += stride) push_edge(a, u, e);
+}
+
+// grid-wide pass over the huge CTA-stage ranges queued by b_push_etwc
+template <class Op>
+__device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
+  const int64_t n = (int64_t)*((volatile unsigned long long*)a.huge_n);
+  const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = 0; k < n; ++k) {
+    const EtwcEntry c = a.huge[k];
+    push_range_strided(a, c.u, c.lo, c.hi(), first, stride);
+  }
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_push_huge(PushArgs<Op> a) {
+  b_push_huge<Op>(a);
+}
 
 template <class Op>
 __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
@@ -453,6 +497,10 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
     int64_t e0 = size - e2 - e1;
     EtwcEntry c2{start, (int32_t)e2, u}, c1{start + e2, (int32_t)e1, u},
         c0{start + e2 + e1, (int32_t)e0, u};
+    if (a.huge && e2 >= kEtwcHuge) {  // whole-grid pass after this kernel / phase
+      a.huge[atomicAdd(a.huge_n, 1ULL)] = c2;
+      e2 = 0;
+    }
     bool has[3] = {e0 > 0, e1 > 0, e2 > 0};
     const EtwcEntry* ent[3] = {&c0, &c1, &c2};
 #pragma unroll
@@ -472,12 +520,12 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
     // stage 1: warps
     for (int k = wid; k < s_n[1]; k += nw) {
       EtwcEntry c = s_q[1][k];
-      for (int64_t e = c.lo + lane; e < c.hi(); e += kWarp) push_edge(a, c.u, e);
+      push_range_strided(a, c.u, c.lo, c.hi(), lane, kWarp);
     }
     // stage 2: whole CTA
     for (int k = 0; k < s_n[2]; ++k) {
       EtwcEntry c = s_q[2][k];
-      for (int64_t e = c.lo + threadIdx.x; e < c.hi(); e += blockDim.x) push_edge(a, c.u, e);
+      push_range_strided(a, c.u, c.lo, c.hi(), threadIdx.x, blockDim.x);
     }
     __syncthreads();
   }

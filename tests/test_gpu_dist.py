@@ -102,9 +102,9 @@ def test_bfs_virtual_ranks_levels_and_tree(nparts, theta):
         parents, st = bfs_virtual(g, nparts, source, theta)
         _levels_and_tree(gg, g, parents, source, off, nbr)
         if theta == 1e-9:
-            assert set(st.direction_log) <= {1}
+            assert set(st.direction_log) <= {"PULL"}
         if theta == 0.999999:
-            assert set(st.direction_log) == {0}
+            assert set(st.direction_log) == {"PUSH"}
 
 
 def test_bfs_dist_single_rank_matches_oracle():
