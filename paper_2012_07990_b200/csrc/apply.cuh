@@ -38,8 +38,10 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
     case GG_LB_ETWC: {
       etwc_huge(rt, &a.huge, &a.huge_n);
       k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
-      k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
-      count_launch();
+      if (a.huge) {
+        k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+        count_launch();
+      }
       break;
     }
     case GG_LB_STRICT: {

@@ -323,6 +323,12 @@ void check_binding(const gg_binding& b) {
 // Dispatch
 // ---------------------------------------------------------------------------
 void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n) {
+  rt->g->ensure_out();
+  if (rt->g->max_out_degree < kEtwcHuge) {  // no hub: no grid pass (no extra barriers)
+    *q = nullptr;
+    *n = nullptr;
+    return;
+  }
   const int64_t cap = rt->g->E / kEtwcHuge + 1;
   if (rt->etwc_q.n < (size_t)cap) rt->etwc_q.alloc(cap);
   if (!rt->etwc_n.p) rt->etwc_n.alloc(1);

@@ -125,6 +125,14 @@ static void build_csr(int dev, int64_t V, int64_t E, const int32_t* keys, const 
   offsets_from_sorted(dev, sorted.p, E, V, off.p, s);
 }
 
+__global__ void k_max_degree(const int64_t* off, int64_t V, unsigned long long* mx) {
+  unsigned long long m = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(off[v + 1] - off[v]));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(mx, m);
+}
+
 void Graph::ensure_out() const {
   Graph& g = const_cast<Graph&>(*this);
   std::lock_guard<std::mutex> lk(g.view_mu);
@@ -133,6 +141,15 @@ void Graph::ensure_out() const {
   DeviceGuard guard(g.dev);
   build_csr(g.dev, g.V, g.E, g.coo_src.p, g.coo_dst.p, g.coo_w.p, g.weighted, g.out_off, g.out_nbr,
             g.out_w, 0);
+  {
+    DevBuf<unsigned long long> mx(1);
+    mx.zero();
+    k_max_degree<<<grid_for(g.V, 256, g.dev), 256>>>(g.out_off.p, g.V, mx.p);
+    GG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    GG_CUDA(cudaMemcpy(&h, mx.p, 8, cudaMemcpyDeviceToHost));
+    g.max_out_degree = (int64_t)h;
+  }
   GG_CUDA(cudaStreamSynchronize(0));
   g.has_out = true;
 }

@@ -35,6 +35,7 @@ struct Graph {
   // CSR views are built on first use (a schedule that only streams the COO
   // never pays for the transpose); guarded by view_mu.
   bool has_out = false, has_in = false;
+  int64_t max_out_degree = -1;  // set when CSR-out is built
   std::mutex view_mu;
   void ensure_out() const;
   void ensure_in() const;

@@ -327,8 +327,18 @@ static PrBlockLayout* layout_for(const Graph& gc, int64_t ns, int ct_bytes, PrPa
 
 int64_t pr_block_window(const Graph& g, int ct_bytes, int64_t blocking_size) {
   if (blocking_size > 0) return blocking_size;
-  int64_t ns = l2_bytes(g.dev) * 3 / 8 / ct_bytes;  // ~3/8 of L2 holds one window
+  // one source window in a fraction of the queried L2 (default 6/16; the
+  // rest holds the streamed edges and the destination accumulators);
+  // GG_PR_WINDOW16 overrides the sixteenths
+  int64_t frac16 = 6;
+  if (const char* e = getenv("GG_PR_WINDOW16")) frac16 = std::max(1, std::min(16, atoi(e)));
+  int64_t ns = l2_bytes(g.dev) * frac16 / 16 / ct_bytes;
   if (ns < 1) ns = 1;
+  // the sort key (segment | destination | source) must fit 64 bits, with one
+  // spare segment id for a partitioned run's foreign edges: widen the window
+  // when a small L2 share would need too many segments
+  const int nvb = nbits((uint64_t)(g.V > 1 ? g.V - 1 : 1));
+  while (32 + nvb + nbits((uint64_t)((g.V + ns - 1) / ns)) > 64) ns *= 2;
   return ns < g.V ? ns : (g.V > 0 ? g.V : 1);
 }
 
