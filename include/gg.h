@@ -123,6 +123,10 @@ typedef struct gg_blocked gg_blocked;   /* device EdgeBlocking layout        */
 const char* gg_last_error(void);
 const char* gg_version(void);
 int gg_device_count(int32_t* count);
+/* Device buffers come from a per-device caching pool (per-query buffers are
+ * reused across calls instead of cudaMalloc/cudaFree each time); this
+ * returns every cached block to the driver.  GG_POOL_MAX_GB caps the cache. */
+int gg_release_cached_memory(void);
 int gg_device_info_get(int32_t device, gg_device_info* info);
 
 /* ---- graph (graphio.Graph.from_coo, graphio.py:58-81) ------------------------

@@ -118,6 +118,7 @@ SIGNATURES = {
     "gg_bc": (I32, [VP, VP, I64, C.POINTER(GGBinding), C.POINTER(GGExec), VP,
                     C.POINTER(GGStats)]),
     "gg_nccl_unique_id": (I32, [VP]),
+    "gg_release_cached_memory": (I32, []),
     "gg_comm_init": (I32, [I32, I32, I32, VP, PP]),
     "gg_comm_destroy": (I32, [VP]),
     "gg_pagerank_dist": (I32, [VP, VP, I64, F64, F64, VP, C.POINTER(GGStats)]),

@@ -134,6 +134,12 @@ struct CallTimer {
 extern "C" {
 
 const char* gg_last_error(void) { return t_err.c_str(); }
+int gg_release_cached_memory(void) {
+  GG_API_BEGIN
+  pool_trim();
+  GG_API_END
+}
+
 const char* gg_version(void) { return "gg-b200 0.1.0 (sm_100a)"; }
 
 int gg_device_count(int32_t* count) {

@@ -34,7 +34,12 @@ __global__ void k_pointer_jump(int32_t* label, int64_t V, int* moved) {
 __global__ void k_cc_first(const int32_t* label, int64_t V, int32_t* first) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
        v += (int64_t)gridDim.x * blockDim.x)
-    atomicMin(first + label[v], (int32_t)v);
+  {
+    // read before the atomic: a giant component's members all share one
+    // label, and an unconditional atomicMin per member serialises on it
+    const int32_t l = label[v];
+    if ((int32_t)v < *((volatile int32_t*)first + l)) atomicMin(first + l, (int32_t)v);
+  }
 }
 __global__ void k_cc_canon(const int32_t* label, const int32_t* first, int64_t V, int32_t* out) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;

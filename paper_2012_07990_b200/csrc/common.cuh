@@ -54,30 +54,46 @@ int64_t launches_now();
 // ---------------------------------------------------------------------------
 // Device buffer (RAII, cudaMalloc on the current device)
 // ---------------------------------------------------------------------------
+// Device memory comes from a per-device caching pool (engine.cu): freed
+// blocks are kept by size class and handed out again, so the per-call
+// buffers of a query (parents, frontiers, marks, queues) cost no
+// cudaMalloc/cudaFree -- which synchronise the device and take milliseconds
+// for GB-sized blocks.  All library work is ordered on the legacy default
+// stream, so a block freed after its last use can be reused by later work.
+void* pool_alloc(size_t bytes, size_t* granted);
+void pool_free(void* p, size_t granted);
+void pool_trim();  // return every cached block to the driver
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t granted = 0;
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), granted(o.granted) { o.p = nullptr; o.n = 0; o.granted = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; granted = o.granted;
+      o.p = nullptr; o.n = 0; o.granted = 0;
+    }
     return *this;
   }
   ~DevBuf() { release(); }
   void alloc(size_t count) {
     release();
     if (count == 0) count = 1;  // keep a valid pointer for empty arrays
-    GG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    p = static_cast<T*>(pool_alloc(count * sizeof(T), &granted));
     n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p, granted);
     p = nullptr;
     n = 0;
+    granted = 0;
   }
   void zero(cudaStream_t s = 0) { if (p) GG_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
   T* get() const { return p; }

@@ -1,3 +1,5 @@
+#include <map>
+#include <mutex>
 // engine.cu — edgeset.apply dispatcher, device frontiers and per-query runtime.
 //
 // Reference anchors (all in /root/reference/pkg/src/schedge/):
@@ -322,6 +324,101 @@ void check_binding(const gg_binding& b) {
 // ---------------------------------------------------------------------------
 // Dispatch
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Caching device allocator (see common.cuh)
+// ---------------------------------------------------------------------------
+namespace {
+struct DevicePool {
+  std::mutex mu;
+  std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;
+  size_t cached = 0;
+};
+DevicePool& pool() {
+  static DevicePool* p = new DevicePool;  // never destroyed: frees at exit are unordered
+  return *p;
+}
+size_t size_class(size_t bytes) {
+  if (bytes <= (1u << 20)) {
+    size_t c = 256;
+    while (c < bytes) c <<= 1;
+    return c;
+  }
+  const size_t g = 2u << 20;
+  return (bytes + g - 1) / g * g;
+}
+// cache at most this many bytes (beyond it, frees go to the driver)
+size_t pool_limit() {
+  static size_t lim = [] {
+    const char* e = getenv("GG_POOL_MAX_GB");
+    return (size_t)(e ? atof(e) : 48.0) * (size_t(1) << 30);
+  }();
+  return lim;
+}
+}  // namespace
+
+void pool_trim() {
+  DevicePool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : P.free_blocks) {
+    cudaSetDevice(kv.first.first);
+    for (void* q : kv.second) cudaFree(q);
+  }
+  cudaSetDevice(cur);
+  P.free_blocks.clear();
+  P.cached = 0;
+}
+
+void* pool_alloc(size_t bytes, size_t* granted) {
+  const size_t c = size_class(bytes);
+  int dev = 0;
+  GG_CUDA(cudaGetDevice(&dev));
+  DevicePool& P = pool();
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.free_blocks.find({dev, c});
+    if (it != P.free_blocks.end() && !it->second.empty()) {
+      void* q = it->second.back();
+      it->second.pop_back();
+      P.cached -= c;
+      *granted = c;
+      return q;
+    }
+  }
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, c);
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    pool_trim();
+    e = cudaMalloc(&q, c);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(GG_ERR_CUDA, strf("cudaMalloc(%zu) failed: %s", c, cudaGetErrorString(e)));
+  }
+  *granted = c;
+  return q;
+}
+
+void pool_free(void* q, size_t granted) {
+  if (!q) return;
+  int dev = 0;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, q) == cudaSuccess) dev = at.device;
+  else if (cudaGetDevice(&dev) != cudaSuccess) return;
+  DevicePool& P = pool();
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.cached + granted <= pool_limit()) {
+      P.free_blocks[{dev, granted}].push_back(q);
+      P.cached += granted;
+      return;
+    }
+  }
+  cudaFree(q);
+}
+
 void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n) {
   rt->g->ensure_out();
   if (rt->g->max_out_degree < kEtwcHuge) {  // no hub: no grid pass (no extra barriers)
