@@ -165,7 +165,14 @@ def cc_bc_c4(gg, args, peak):
     bc_sources = _pick_sources(deg, args.sources or 4, 6)
     cc_res, bc_res = {}, {}
     for lb in lbs:
-        prog = gg.ScheduleProgram({"s0:s1": gg.Schedule(direction="PUSH", load_balance=lb)})
+        # "EB" = EDGE_ONLY + BLOCKED (EdgeBlocking, blocking.py:78-186), "EDGE" = EDGE_ONLY
+        if lb == "EB":
+            sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True)
+        elif lb == "EDGE":
+            sch = gg.Schedule(load_balance="EDGE_ONLY")
+        else:
+            sch = gg.Schedule(direction="PUSH", load_balance=lb)
+        prog = gg.ScheduleProgram({"s0:s1": sch})
         for _ in range(max(1, min(args.warmup, 2))):
             gg.cc_soman(g, prog, out=labels)
         ms, st = [], None
@@ -177,6 +184,8 @@ def cc_bc_c4(gg, args, peak):
         cc_res[lb] = {"ms": m, "rounds": st.rounds, "edges_traversed": st.edges_traversed,
                       "gteps": st.edges_traversed / (m * 1e-3) / 1e9,
                       "frac": ((4.0 * A + 16.0 * V) * st.rounds / (m * 1e-3) / 1e9) / peak}
+        if lb in ("EB", "EDGE"):  # frontier traversals: EDGE_ONLY would scan every arc per level
+            continue
         gg.bc(g, bc_sources[:1], prog, out=scores)
         r = gg.bc(g, bc_sources, prog, out=scores)
         bm = r.stats.kernel_ms
@@ -188,7 +197,7 @@ def cc_bc_c4(gg, args, peak):
     m_c = []
     for s in bc_sources:
         m_c.append(int(deg[lab == lab[s]].sum()) // 2)
-    for lb in lbs:
+    for lb in bc_res:
         bc_res[lb]["gteps"] = 2.0 * sum(m_c) / (bc_res[lb]["ms"] * 1e-3) / 1e9
     if args.check:
         import oracle

@@ -9,23 +9,24 @@
 // So the B200 blocking confines the *random* side of the gather formulation
 // to the L2 instead:
 //
-//   preprocessing (once per graph and window, cached):
-//     1. renumber vertices by out-degree, descending (hot sources first);
+//   preprocessing (once per graph and window, cached; prblock build_layout):
+//     1. out-degree histogram of the COO (warp-aggregated atomics) and a
+//        renumbering by out-degree, descending (hot sources first);
 //     2. segment k = sources [k*Ns, (k+1)*Ns), Ns*sizeof(contrib) sized to a
 //        fraction of the queried L2 (blocking_size overrides Ns);
-//     3. stable sort of all edges by (segment, destination, source): inside
-//        a segment each destination's in-edges are contiguous;
-//     4. virtual rows per segment (long rows split into hub pieces), every
-//        segment padded to whole 32-row warp chunks.  Segment 0 (the hot
-//        sources, ~94% of RMAT-27 edges) lists *every* destination.
+//     3. stable radix sort of the edges by (segment, destination) with the
+//        source as payload (32-bit keys when they fit): inside a segment each
+//        destination's in-edges are contiguous, in COO order;
 //   per iteration (Alg. 2: segments in order, a barrier between them):
-//     cold segments k = 1..K-1: warp-per-32-rows gather from the segment's
-//       L2-resident contrib window, row sums added to acc[dst];
-//     hot segment 0 last: gather + acc + fused vertex update (rank, L1,
-//       dangling mass, next contrib) and acc reset; hub pass finishes split rows.
+//     cold segments k = 1..K-1: edge-parallel gather from the segment's
+//       L2-resident contrib window, destination runs reduced in registers
+//       (warp segmented scan), one f64 add per run;
+//     hot segment 0 last: the same with the hottest sources' contributions
+//       staged in shared memory (128 KB; the rest of the array stays L1,
+//       which stages the in-flight gather lines); then the vertex pass.
 // All per-vertex state lives in the renumbered id space; ranks are permuted
 // back on output.  Results equal the reference's up to f64 summation order.
-#include "prtile.cuh"
+#include "prtile.cuh"  // block_sum
 #include "apply.cuh"
 #include "prdist.cuh"
 #include <cub/device/device_radix_sort.cuh>
@@ -43,16 +44,14 @@ struct PrPart {
 };
 
 struct PrBlockLayout {
-  int64_t ns = 0, K = 0, V = 0, E = 0, nrows = 0;
+  int64_t ns = 0, K = 0, V = 0, E = 0;
   int ct_bytes = 0;
   int P = 1, r = 0;
   int64_t lo = 0, hi = 0;                            // owned destinations (renumbered ids)
   std::vector<int64_t> bounds;                       // P+1 partition bounds (renumbered ids)
-  DevBuf<int32_t> newid, order, outdeg, src, owner;  // owner: cold pair -> destination
+  DevBuf<int32_t> newid, order, outdeg, src;         // src: renumbered sources, blocked order
   DevBuf<int32_t> dst;                               // local destination of every blocked edge
   std::vector<int64_t> seg_edge;                     // K+1 edge boundaries (segment 0 = hot)
-  DevBuf<int64_t> roff;                              // all rows: hot [0,Vloc) then cold pairs
-  std::vector<int64_t> seg_row;                      // K+1 row boundaries (segment 0 = hot)
   double prep_ms = 0;
   int64_t vloc() const { return hi - lo; }
   // per-run work buffers, kept across calls (cudaMalloc/cudaFree of GB-sized
@@ -68,37 +67,77 @@ static int nbits(uint64_t x) {
   return b ? b : 1;
 }
 
-__global__ void k_neg_deg(const int64_t* off, int64_t V, uint32_t* key, int32_t* ids) {
+// out-degree histogram; lanes holding the same source (runs in source-sorted
+// input, hubs in any order) add once per group
+__global__ void k_outdeg_hist(const int32_t* s, int64_t E, uint32_t* deg) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); base < E; base += stride) {
+    const int64_t e = base + lane_id();
+    const int32_t u = e < E ? s[e] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, u);
+    if (u >= 0 && lane_id() == __ffs(grp) - 1) atomicAdd(deg + u, (uint32_t)__popc(grp));
+  }
+}
+__global__ void k_neg_deg(const uint32_t* deg, int64_t V, uint32_t* key, int32_t* ids) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
        v += (int64_t)gridDim.x * blockDim.x) {
-    key[v] = ~(uint32_t)(off[v + 1] - off[v]);
+    key[v] = ~deg[v];
     ids[v] = (int32_t)v;
   }
 }
-__global__ void k_relabel_tables(const int32_t* order, const int64_t* off, int64_t V, int32_t* newid,
+__global__ void k_relabel_tables(const int32_t* order, const uint32_t* deg, int64_t V, int32_t* newid,
                                  int32_t* outdeg_new) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t o = order[i];
     newid[o] = (int32_t)i;
-    outdeg_new[i] = (int32_t)(off[o + 1] - off[o]);
+    outdeg_new[i] = (int32_t)deg[o];
   }
 }
-// key = (source segment, local destination, source); edges whose
-// destination another rank owns get segment K (sorted past every kept edge).
+// key = (source segment, local destination), payload = renumbered source;
+// edges whose destination another rank owns get segment K (sorted last).
+template <class KT>
 __global__ void k_edge_keys(const int32_t* s, const int32_t* d, int64_t E, const int32_t* newid,
-                            int64_t ns, int nvb, int64_t lo, int64_t hi, uint64_t K, uint64_t* key) {
+                            int64_t ns, int nvb, int64_t lo, int64_t hi, uint64_t K, KT* key, int32_t* val) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t nu = (uint32_t)newid[s[e]];
-    int64_t nv = newid[d[e]];
+    const int32_t nu = newid[s[e]];
+    const int64_t nv = newid[d[e]];
+    val[e] = nu;
     if (nv < lo || nv >= hi) {
-      key[e] = K << (32 + nvb);
+      key[e] = (KT)(K << nvb);
       continue;
     }
-    uint64_t k = nu / (uint64_t)ns;
-    key[e] = (k << (32 + nvb)) | ((uint64_t)(nv - lo) << 32) | nu;
+    key[e] = (KT)((((uint64_t)nu / (uint64_t)ns) << nvb) | (uint64_t)(nv - lo));
   }
+}
+template <class KT>
+__global__ void k_count_hot(const KT* key, int64_t E, int shift, unsigned long long* n) {
+  unsigned long long c = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x)
+    c += ((uint64_t)key[e] >> shift) == 0;
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(n, c);
+}
+template <class KT>
+__global__ void k_dst_of_keys(const KT* key, int64_t E, int nvb, int32_t* dst) {
+  const uint64_t mask = (1ULL << nvb) - 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = (int32_t)((uint64_t)key[e] & mask);
+}
+// first edge of each segment (segments are sorted): seg_edge[k] = lower bound
+template <class KT>
+__global__ void k_seg_bounds(const KT* key, int64_t E, int shift, int64_t K, int64_t* seg_edge) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > K) return;
+  int64_t a = 0, b = E;
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if ((int64_t)((uint64_t)key[mid] >> shift) < k) a = mid + 1; else b = mid;
+  }
+  seg_edge[k] = a;
 }
 // in-degree per renumbered vertex (partition balance)
 __global__ void k_indeg_new(const int32_t* d, int64_t E, const int32_t* newid, unsigned long long* cnt) {
@@ -122,52 +161,6 @@ __global__ void k_part_bounds(const unsigned long long* in_off, int64_t V, int P
   }
   bounds[r] = lo & ~int64_t(31);
 }
-__global__ void k_split_keys(const uint64_t* key, int64_t E, int nvb, int32_t* src, int32_t* dst_hot,
-                             int64_t E0) {
-  const uint64_t mask = (1ULL << nvb) - 1;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = key[e];
-    src[e] = (int32_t)(k & 0xffffffffULL);
-    if (e < E0) dst_hot[e] = (int32_t)((k >> 32) & mask);
-  }
-}
-struct IsCold {
-  const uint64_t* key;
-  int shift;
-  __device__ __forceinline__ bool operator()(int64_t e) const { return (key[e] >> shift) != 0; }
-};
-__global__ void k_dst_of_keys(const uint64_t* key, int64_t E, int nvb, int32_t* dst) {
-  const uint64_t mask = (1ULL << nvb) - 1;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x)
-    dst[e] = (int32_t)((key[e] >> 32) & mask);
-}
-__global__ void k_count_hot(const uint64_t* key, int64_t E, int shift, unsigned long long* n) {
-  unsigned long long c = 0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x)
-    c += (key[e] >> shift) == 0;
-  c = warp_sum(c);
-  if (lane_id() == 0 && c) atomicAdd(n, c);
-}
-// cold run starts: positions e in [E0, E) where (segment, dst) changes
-struct RunStart {
-  const uint64_t* key;
-  int64_t E0;
-  __device__ __forceinline__ bool operator()(int64_t e) const {
-    return e == E0 || (key[e] >> 32) != (key[e - 1] >> 32);
-  }
-};
-__global__ void k_pieces(const int64_t* start, int64_t n, int64_t end, int64_t hub_t, int64_t* pieces,
-                         int min1) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t len = (p + 1 < n ? start[p + 1] : end) - start[p];
-    int64_t q = (len + hub_t - 1) / hub_t;
-    pieces[p] = q < 1 ? (min1 ? 1 : 0) : q;
-  }
-}
 template <class T>
 static T dget(const T* p) {
   T h;
@@ -175,18 +168,40 @@ static T dget(const T* p) {
   return h;
 }
 
-__global__ void k_pair_owner(const uint64_t* key, const int64_t* pstart, int64_t n, int nvb, int32_t* owner) {
-  const uint64_t mask = (1ULL << nvb) - 1;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x)
-    owner[p] = (int32_t)((key[pstart[p]] >> 32) & mask);
+
+template <class KT>
+static void sort_edges(const Graph& g, PrBlockLayout* L, int nvb, int kb, int64_t E) {
+  const int dev = g.dev;
+  const int64_t Eall = g.E;
+  const int shift = nvb;
+  DevBuf<KT> keys(Eall);
+  {
+    DevBuf<KT> k0(Eall);
+    DevBuf<int32_t> v0(Eall);
+    L->src.alloc(Eall);  // payload: renumbered sources in (segment, destination) order
+    k_edge_keys<KT><<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, Eall, L->newid.p, L->ns, nvb,
+                                                       L->lo, L->hi, (uint64_t)L->K, k0.p, v0.p);
+    GG_LAUNCH_CHECK();
+    size_t temp = 0;
+    GG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0.p, keys.p, v0.p, L->src.p, Eall, 0, nvb + kb));
+    DevBuf<uint8_t> tb(temp);
+    GG_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, temp, k0.p, keys.p, v0.p, L->src.p, Eall, 0, nvb + kb));
+  }
+  L->src.n = E;  // foreign edges (partitioned run) sort past E
+  L->dst.alloc(E);
+  k_dst_of_keys<KT><<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->dst.p);
+  DevBuf<int64_t> se(L->K + 1);
+  k_seg_bounds<KT><<<(unsigned)((L->K + 1 + 127) / 128), 128>>>(keys.p, E, shift, L->K, se.p);
+  GG_LAUNCH_CHECK();
+  L->seg_edge.resize(L->K + 1);
+  GG_CUDA(cudaMemcpy(L->seg_edge.data(), se.p, (L->K + 1) * 8, cudaMemcpyDeviceToHost));
+  L->seg_edge[L->K] = E;
 }
 
 static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, int ct_bytes, PrPart part) {
   const int dev = g.dev;
   const int64_t V = g.V, Eall = g.E;
   if (!g.has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
-  CsrView out = g.out_view();
   auto L = std::make_shared<PrBlockLayout>();
   double t0 = now_ms();
   L->ns = ns;
@@ -195,12 +210,15 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   L->ct_bytes = ct_bytes;
   L->P = part.P;
   L->r = part.r;
-  // 1. out-degree renumbering (stable, descending)
+  // 1. out-degree renumbering (stable, descending), from a COO histogram
   {
-    DevBuf<uint32_t> key(V), key2(V);
+    DevBuf<uint32_t> deg(V), key(V), key2(V);
     DevBuf<int32_t> ids(V);
+    deg.zero();
+    k_outdeg_hist<<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, Eall, deg.p);
     L->order.alloc(V);
-    k_neg_deg<<<grid_for(V, 256, dev), 256>>>(out.off, V, key.p, ids.p);
+    k_neg_deg<<<grid_for(V, 256, dev), 256>>>(deg.p, V, key.p, ids.p);
+    GG_LAUNCH_CHECK();
     if (getenv("GG_PR_NO_RELABEL")) GG_CUDA(cudaMemset(key.p, 0, V * sizeof(uint32_t)));  // ablation
     size_t temp = 0;
     GG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, key.p, key2.p, ids.p, L->order.p, V));
@@ -208,7 +226,7 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
     GG_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, temp, key.p, key2.p, ids.p, L->order.p, V));
     L->newid.alloc(V);
     L->outdeg.alloc(V);
-    k_relabel_tables<<<grid_for(V, 256, dev), 256>>>(L->order.p, out.off, V, L->newid.p, L->outdeg.p);
+    k_relabel_tables<<<grid_for(V, 256, dev), 256>>>(L->order.p, deg.p, V, L->newid.p, L->outdeg.p);
     GG_LAUNCH_CHECK();
   }
   // 1b. destination partition in the renumbered id space, balanced by in-edges
@@ -238,76 +256,12 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   const int64_t Vl = L->hi - L->lo;
   const int nvb = nbits((uint64_t)(Vl > 1 ? Vl - 1 : 1));
   const int kb = nbits((uint64_t)L->K);  // segment K marks edges of other ranks
-  if (32 + nvb + kb > 64) fail(GG_ERR_VALUE, "EdgeBlocking layout: too many segments for this graph");
-  // 2-3. (segment, dst, src) keys, sorted; other ranks' edges sort last
-  DevBuf<uint64_t> keys(Eall);
-  {
-    DevBuf<uint64_t> k0(Eall);
-    k_edge_keys<<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, Eall, L->newid.p, ns, nvb, L->lo,
-                                                   L->hi, (uint64_t)L->K, k0.p);
-    GG_LAUNCH_CHECK();
-    size_t temp = 0;
-    GG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, k0.p, keys.p, Eall, 0, 32 + nvb + kb));
-    DevBuf<uint8_t> tb(temp);
-    GG_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, temp, k0.p, keys.p, Eall, 0, 32 + nvb + kb));
-  }
-  const int shift = 32 + nvb;
-  DevBuf<unsigned long long> cnt(1);
-  cnt.zero();
-  k_count_hot<<<grid_for(E, 256, dev), 256>>>(keys.p, E, shift, cnt.p);
-  GG_LAUNCH_CHECK();
-  const int64_t E0 = (int64_t)dget(cnt.p);
-  // 4. rows: [0, Vl) hot (local) destinations (CSR over the hot edges), then
-  //    the cold (segment, destination) pairs; one offsets array for all rows.
-  L->src.alloc(E);
-  L->dst.alloc(E);
-  k_dst_of_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->dst.p);
-  GG_LAUNCH_CHECK();
-  const int64_t Ec = E - E0;
-  DevBuf<int64_t> pstart(Ec + 1);
-  DevBuf<unsigned long long> npairs(1);
-  npairs.zero();
-  int64_t P = 0;
-  if (Ec > 0) {
-    cub::CountingInputIterator<int64_t> it(E0);
-    RunStart pred{keys.p, E0};
-    size_t temp = 0;
-    GG_CUDA(cub::DeviceSelect::If(nullptr, temp, it, pstart.p, npairs.p, Ec, pred));
-    DevBuf<uint8_t> tb(temp);
-    GG_CUDA(cub::DeviceSelect::If(tb.p, temp, it, pstart.p, npairs.p, Ec, pred));
-    P = (int64_t)dget(npairs.p);
-  }
-  L->nrows = Vl + P;
-  L->roff.alloc(Vl + P + 1);
-  {
-    DevBuf<int32_t> dh(E0 > 0 ? E0 : 1);
-    k_split_keys<<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->src.p, dh.p, E0);
-    GG_LAUNCH_CHECK();
-    offsets_from_sorted(dev, dh.p, E0, Vl, L->roff.p, 0);  // roff[0..Vl], roff[Vl] = E0
-  }
-  if (P > 0) {
-    GG_CUDA(cudaMemcpy(L->roff.p + Vl, pstart.p, P * 8, cudaMemcpyDeviceToDevice));
-    L->owner.alloc(P);
-    k_pair_owner<<<grid_for(P, 256, dev), 256>>>(keys.p, pstart.p, P, nvb, L->owner.p);
-    GG_LAUNCH_CHECK();
-  }
-  GG_CUDA(cudaMemcpy(L->roff.p + Vl + P, &E, 8, cudaMemcpyHostToDevice));
-  // segment row ranges: cold pairs are sorted by segment; find boundaries by
-  // binary search through the pair keys (K is small)
-  L->seg_row.assign(L->K + 1, Vl + P);
-  L->seg_row[0] = 0;
-  if (L->K > 1) L->seg_row[1] = Vl;
-  for (int64_t k = 2; k < L->K; ++k) {
-    int64_t lo = 0, hi = P;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) / 2;
-      int64_t e = dget(pstart.p + mid);
-      if ((int64_t)(dget(keys.p + e) >> shift) < k) lo = mid + 1; else hi = mid;
-    }
-    L->seg_row[k] = Vl + lo;
-  }
-  L->seg_edge.resize(L->K + 1);
-  for (int64_t k = 0; k <= L->K; ++k) L->seg_edge[k] = dget(L->roff.p + L->seg_row[k]);
+  if (nvb + kb > 64) fail(GG_ERR_VALUE, "EdgeBlocking layout: too many segments for this graph");
+  // 2-3. (segment, destination) keys with the source as payload, stably sorted
+  if (nvb + kb <= 32)
+    sort_edges<uint32_t>(g, L.get(), nvb, kb, E);
+  else
+    sort_edges<uint64_t>(g, L.get(), nvb, kb, E);
   GG_CUDA(cudaDeviceSynchronize());
   L->prep_ms = now_ms() - t0;
   return L;
@@ -334,11 +288,11 @@ int64_t pr_block_window(const Graph& g, int ct_bytes, int64_t blocking_size) {
   if (const char* e = getenv("GG_PR_WINDOW16")) frac16 = std::max(1, std::min(16, atoi(e)));
   int64_t ns = l2_bytes(g.dev) * frac16 / 16 / ct_bytes;
   if (ns < 1) ns = 1;
-  // the sort key (segment | destination | source) must fit 64 bits, with one
+  // the sort key (segment | destination) must fit 64 bits, with one
   // spare segment id for a partitioned run's foreign edges: widen the window
   // when a small L2 share would need too many segments
   const int nvb = nbits((uint64_t)(g.V > 1 ? g.V - 1 : 1));
-  while (32 + nvb + nbits((uint64_t)((g.V + ns - 1) / ns)) > 64) ns *= 2;
+  while (nvb + nbits((uint64_t)((g.V + ns - 1) / ns)) > 64) ns *= 2;
   return ns < g.V ? ns : (g.V > 0 ? g.V : 1);
 }
 
