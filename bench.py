@@ -62,7 +62,8 @@ def parse():
     p.add_argument("--cpu-scale", type=int, default=22)
     # c2-c4 (bench_algos.py)
     p.add_argument("--sources", type=int, default=None)
-    p.add_argument("--theta", type=float, default=0.05, help="c2 hybrid threshold")
+    p.add_argument("--theta", type=float, default=0.0005, help="c2 hybrid threshold (swept: best)")
+    p.add_argument("--no-dedup", action="store_true", help="c2: s1 without dedup (CAS already dedups)")
     p.add_argument("--pull-lb", default="VERTEX_BASED", help="c2 pull-side load balance")
     p.add_argument("--fusion", action="store_true", help="c2: fused loop")
     p.add_argument("--side", type=int, default=None, help="c3 grid side")

@@ -246,3 +246,50 @@ def test_algorithm_errors(gg, graphs):
     with pytest.warns(UserWarning, match="symmetrizing"):
         r = gg.cc_soman(gg.Graph.from_coo(6, [0, 1, 2, 3, 4, 5], [1, 2, 0, 4, 5, 3]))
     assert r.values == [0, 0, 0, 3, 3, 3]
+
+
+# ---------------------------------------------------------------------------
+# hubs above the ETWC grid-pass threshold (CTA-stage ranges >= 16384 arcs go
+# to k_push_huge / the fused grid pass): stars + a random background
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def hub_graph(gg):
+    rng = np.random.default_rng(11)
+    V = 60000
+    hubs = [0, 7, 31]
+    src, dst = [], []
+    for h, deg in zip(hubs, [40000, 20000, 17000]):
+        nb = rng.choice(np.arange(100, V), size=deg, replace=False)
+        src.append(np.full(deg, h)); dst.append(nb)
+    s = rng.integers(100, V, 50000); d = rng.integers(100, V, 50000)
+    src.append(s); dst.append(d)
+    s = np.concatenate(src).astype(np.int64); d = np.concatenate(dst).astype(np.int64)
+    keep = s != d
+    s, d = s[keep], d[keep]
+    from paper_2012_07990_b200.graphio import symmetrize_coo
+    s2, d2, _, _ = symmetrize_coo(s, d)
+    g = gg.Graph.from_coo(V, s2, d2, symmetric=True)
+    off, nbr, _ = oracle.csr(V, g.coo_src, g.coo_dst)
+    return g, off, nbr
+
+
+@pytest.mark.parametrize("fusion", [False, True])
+def test_etwc_hub_pass_bfs_cc(gg, hub_graph, fusion):
+    g, off, nbr = hub_graph
+    V = g.num_vertices
+    assert int(np.max(np.diff(off))) >= 16384
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance="ETWC"), fusion=fusion)
+    for src in (0, 7, 150):
+        r = gg.bfs(g, src, prog)
+        assert gg.bfs_levels(r.values) == oracle.bfs_levels(V, off, nbr, src).tolist()
+        legal_bfs_tree(g, r.values, src)
+        assert r.stats.edges_traversed == int(sum(np.diff(off)[np.asarray(r.values) >= 0]))
+    want, _ = oracle.cc(V, g.coo_src, g.coo_dst)
+    assert np.array_equal(gg.cc_soman(g, prog).array, want)
+
+
+def test_etwc_hub_pass_bc(gg, hub_graph):
+    g, off, nbr = hub_graph
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance="ETWC"))
+    srcs = [0, 150, 7]
+    close_bc(gg.bc(g, srcs, prog).values, oracle.bc(g.num_vertices, off, nbr, srcs))
