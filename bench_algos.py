@@ -53,7 +53,7 @@ def bfs_c2(gg, args, peak):
     theta = args.theta
     hy = gg.HybridSchedule(threshold=theta,
                            s1=gg.Schedule(direction="PUSH", load_balance="ETWC",
-                                          dedup=not args.no_dedup),
+                                          dedup=args.dedup),
                            s2=gg.Schedule(direction="PULL", pull_frontier_repr="BITMAP",
                                           frontier_creation="UNFUSED_BITMAP",
                                           load_balance=args.pull_lb))
@@ -88,7 +88,7 @@ def bfs_c2(gg, args, peak):
     line = {"value": _hmean(teps), "ms_per_step": med_ms, "steps": len(sources),
             "config": {"workload": "bfs_do_etwc_rmat%d_ef16_sym" % scale, "V": V, "arcs": A,
                        "sources": len(sources), "source_seed": 3,
-                       "schedule": {"s1": "PUSH+ETWC" + ("+DEDUP_DISABLED" if args.no_dedup else ""),
+                       "schedule": {"s1": "PUSH+ETWC" + ("" if args.dedup else "+DEDUP_DISABLED"),
                                     "s2": "PULL+BITMAP+UNFUSED_BITMAP+%s" % args.pull_lb,
                                     "threshold": theta,
                                     "kernel_fusion": bool(args.fusion)},

@@ -116,6 +116,9 @@ struct OpHook {
     int32_t la = *((volatile int32_t*)label + u), lb = *((volatile int32_t*)label + v);
     if (la == lb) return;
     int32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
+    // skip hooks that cannot lower label[hi] (hub roots receive one hook per
+    // incident arc; only the smaller ones need the atomic)
+    if (lo >= *((volatile int32_t*)label + hi)) return;
     // read before write: one hot flag line, written once per round instead of
     // once per successful hook (which serialises at its L2 slice)
     if (atomicMin(label + hi, lo) > lo && !*((volatile int*)changed)) *changed = 1;
@@ -183,7 +186,8 @@ struct OpBcFwd {
   }
   __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder& out) const {
     const int32_t nl = level + 1;
-    if (atomicCAS(depth + v, -1, nl) == -1) out.emit(v);
+    // the CAS only when v looked unvisited (the filter admitted -1 or nl)
+    if (*((volatile int32_t*)depth + v) == -1 && atomicCAS(depth + v, -1, nl) == -1) out.emit(v);
     if (*((volatile int32_t*)depth + v) == nl) atomicAdd(sigma + v, sigma[u]);
   }
   __device__ __forceinline__ Acc init() const { return {0.0, 0}; }
@@ -224,6 +228,12 @@ struct OpBcBwd {
     if (__ldg(depth + v) == __ldg(depth + u) + 1)
       atomicAdd(delta + u, __ldg(sigma + u) / __ldg(sigma + v) * (1.0 + delta[v]));
   }
+  // range walks accumulate per source and commit once per warp (traverse.cuh)
+  static constexpr bool kPushReduce = true;
+  __device__ __forceinline__ double push_val(int32_t u, int32_t v) const {
+    return __ldg(depth + v) == __ldg(depth + u) + 1 ? __ldg(sigma + u) / __ldg(sigma + v) * (1.0 + delta[v]) : 0.0;
+  }
+  __device__ __forceinline__ void push_commit(int32_t u, double x) const { atomicAdd(delta + u, x); }
   __device__ __forceinline__ Acc init() const { return 0; }
   __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t w) const {
     push(u, v, w, OutBuilder{});

@@ -13,6 +13,7 @@
 // Frontiers: SPARSE int32 queue + u64 device count; BITMAP u32 words (same
 // byte/bit order as the reference's bytearray, frontier.py:184); BOOLMAP u8.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 #include <cooperative_groups.h>
 
@@ -436,11 +437,36 @@ struct EtwcEntry {
 // slice of the active list): such ranges are handed to the whole grid.
 constexpr int64_t kEtwcHuge = 16384;
 
+// Ops whose push is "accumulate into the SOURCE" (BC backward: delta[u] +=
+// f(v)) declare kPushReduce and provide push_val / push_commit: a range walk
+// sums its arcs per thread, reduces over the warp and issues one atomic per
+// warp instead of one per arc on the same address.
+template <class, class = void>
+struct PushReduce : std::false_type {};
+template <class T>
+struct PushReduce<T, std::void_t<decltype(T::kPushReduce)>> : std::integral_constant<bool, T::kPushReduce> {};
+
 // Cooperative range walk with 4 independent arcs in flight per thread.
+// `warp_uniform`: every lane of the warp walks the same source u.
 template <class Op>
 __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_t u, int64_t lo, int64_t hi,
-                                                   int64_t first, int64_t stride) {
+                                                   int64_t first, int64_t stride, bool warp_uniform = true) {
   int64_t e = lo + first;
+  if constexpr (PushReduce<Op>::value) {
+    double acc = 0.0;
+    for (; e < hi; e += stride) {
+      const int32_t v = __ldg(a.g.nbr + e);
+      if (a.use_filter && !a.op.filter(v)) continue;
+      acc += a.op.push_val(u, v);
+    }
+    if (warp_uniform) {
+      acc = warp_sum(acc);
+      if (lane_id() == 0 && acc != 0.0) a.op.push_commit(u, acc);
+    } else if (acc != 0.0) {
+      a.op.push_commit(u, acc);
+    }
+    return;
+  }
   for (; e + 3 * stride < hi; e += 4 * stride) {
     int32_t v[4];
 #pragma unroll
@@ -515,7 +541,7 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
     // stage 0: individual threads
     for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
       EtwcEntry c = s_q[0][k];
-      for (int64_t e = c.lo; e < c.hi(); ++e) push_edge(a, c.u, e);
+      push_range_strided(a, c.u, c.lo, c.hi(), 0, 1, false);
     }
     // stage 1: warps
     for (int k = wid; k < s_n[1]; k += nw) {
