@@ -599,7 +599,9 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
   // at most 128 KB per SM: the rest of the 256 KB L1/shared array stays L1,
   // which stages the in-flight gather lines (measured: 227 KB of cache halves
   // the kernel's gather rate; 128 KB gives the best time at f32 and f64)
-  int smem_per_cta = std::min(smem_max - 2048, 128 * 1024) / h.per_sm;
+  int cap_kb = 128;
+  if (const char* e = getenv("GG_PR_HOT_KB")) cap_kb = std::max(4, atoi(e));
+  int smem_per_cta = std::min(smem_max - 2048, cap_kb * 1024) / h.per_sm;
   int64_t nhot64 = std::min<int64_t>(smem_per_cta / (int)sizeof(CT), L->ns);
   if (const char* nh = getenv("GG_PR_NHOT")) nhot64 = std::min<int64_t>(nhot64, atoll(nh));
   nhot64 &= ~int64_t(3);

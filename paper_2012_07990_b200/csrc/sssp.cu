@@ -90,7 +90,11 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   int cur = 0, take = 1, far = 2, far2 = 3;
   unsigned long long index = 0;
-  long long rounds = 0, relax = 0;
+  long long rounds = 0, relax = 0, advances = 0;
+  // Two grid barriers per round.  Counts are captured in registers right
+  // after the top barrier, so a queue's count can be reset by thread 0 as
+  // soon as nobody reads it any more; the advance's minimum alternates
+  // between two slots, the unused one re-armed for the next advance.
   while (true) {
     grid.sync();
     const unsigned long long ncur = *((volatile unsigned long long*)a.qn + cur);
@@ -99,8 +103,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
     ++rounds;
     if (ncur == 0) {
       // advance(): minimum live far bucket, then split far
-      if (tid == 0) *a.best = kUnreached;
-      grid.sync();
+      unsigned long long* bestp = a.best + (advances & 1);
       unsigned long long b_min = kUnreached;
       for (int64_t i = tid; i < (int64_t)nfar; i += nth) {
         int32_t v = a.q[far][i];
@@ -108,9 +111,9 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
         unsigned long long b = a.dist[v] / a.delta;
         if (b > index && b < b_min) b_min = b;
       }
-      if (b_min != kUnreached) atomicMin(a.best, b_min);
+      if (b_min != kUnreached) atomicMin(bestp, b_min);
       grid.sync();
-      const unsigned long long best = *((volatile unsigned long long*)a.best);
+      const unsigned long long best = *((volatile unsigned long long*)bestp);
       if (best != kUnreached) {
         OutBuilder oc{}, of{};
         oc.mode = of.mode = GG_CREATE_FUSED;
@@ -126,14 +129,17 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
         }
         index = best;
       }
-      grid.sync();
-      if (tid == 0) a.qn[far] = 0;
+      if (tid == 0) {
+        a.qn[far] = 0;                         // count read into registers above
+        a.best[(advances + 1) & 1] = kUnreached;  // next advance's slot
+      }
+      ++advances;
       int t = far; far = far2; far2 = t;
       continue;
     }
-    // take_current(): the pending bucket becomes the relax input
+    // take_current(): the pending bucket becomes the relax input; the new
+    // current queue (the previous input) is no longer read by anyone
     { int t = cur; cur = take; take = t; }
-    grid.sync();
     if (tid == 0) a.qn[cur] = 0;
     for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.cmark[a.q[take][i]] = 0;
     InView iv{};
@@ -156,9 +162,10 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
     OutBuilder none{};
     none.mode = OUT_NONE;
     fused_edge_phase(a.s, a.out, a.out, a.coo, iv, op, none, false, a.scanned, a.sc, a.cta, grid);
-    grid.sync();
-    if (a.s.load_balance == GG_LB_EDGE_ONLY)
+    if (a.s.load_balance == GG_LB_EDGE_ONLY) {
+      grid.sync();  // membership is read by the edge phase
       for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 0;
+    }
     ++relax;
   }
   if (tid == 0) {
@@ -209,8 +216,9 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
     a.dist = dist.p;
     a.delta = delta;
     DevBuf<int32_t> q[4];
-    DevBuf<unsigned long long> qn(4), best(1);
+    DevBuf<unsigned long long> qn(4), best(2);
     qn.zero(st);
+    GG_CUDA(cudaMemsetAsync(best.p, 0xff, 2 * sizeof(unsigned long long), st));
     for (int k = 0; k < 4; ++k) {
       q[k].alloc(V + 1);
       a.q[k] = q[k].p;
