@@ -263,12 +263,16 @@ def main():
         edge_n = 0
         launches = 0
         e_local = 0
+        top_ms, top_n, top_edges = 0.0, 0, 0
         for _ in range(args.steps):
             st = step()
             edge_ms += st.edge_ms
             edge_n += st.edge_launches
             launches += st.gpu_launches
             e_local = st.edges_traversed // iters
+            top_ms += st.top_ms
+            top_n += st.top_launches
+            top_edges = st.top_edges
         ev1.record()
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -279,13 +283,32 @@ def main():
     # strong scaling: the same RMAT-27 graph at every N (partitioned at N > 1)
     value = iters * E / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (edge phase), algorithmic bytes per launch:
-    # 8 B/edge (COO pair) + 16 B/vertex (contrib read, acc write) -- SURVEY §8(d)
+    # roofline (SURVEY §8(d) fixed byte model: 8 B per edge, 16 B per vertex for
+    # the edge phase (contrib read + acc write), 32 B per vertex per iteration).
+    # Dominant kernel = the hot-segment gather (k_pr_edges_hot): its edges x 8 B
+    # + the vertices' 16 B, over its CUDA-event time; the whole edge phase and
+    # the whole iteration are reported beside it.
     avg_edge_ms = edge_ms / max(1, edge_n)
     alg_edge = 8.0 * e_local + 16.0 * V / world  # this rank's share (all of it at N=1)
-    achieved = alg_edge / (avg_edge_ms * 1e-3) / 1e9
+    edge_achieved = alg_edge / (avg_edge_ms * 1e-3) / 1e9
     alg_iter = 8.0 * E + 32.0 * V
     iter_achieved = alg_iter * iters / (ms * 1e-3) / 1e9 / world  # per-GPU share of the aggregate
+    if top_n:
+        avg_top_ms = top_ms / top_n
+        alg_top = 8.0 * top_edges + 16.0 * V / world
+        kernel = "k_pr_edges_hot (hot source segment, %d of %d edges)" % (top_edges, e_local)
+    else:
+        avg_top_ms, alg_top, kernel = avg_edge_ms, alg_edge, "edge phase (%s)" % args.schedule
+    achieved = alg_top / (avg_top_ms * 1e-3) / 1e9
+    # DRAM bytes per launch of that kernel from the committed ncu --set full
+    # capture of this exact configuration (bench can not run ncu itself)
+    traffic, traffic_note = None, "no ncu capture committed for this configuration"
+    if (top_n and args.schedule == "eb" and not args.fp32_contrib and scale == 27
+            and world == 1 and not args.permute):
+        traffic = 16.291855e9 + 0.618621e9
+        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                        "profiles/r01/ncu_full_k_pr_edges_hot_f64.txt (= the streamed "
+                        "edges; the gathers hit L2)")
 
     line = {"metric": metric, "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -301,9 +324,11 @@ def main():
                        "generate_s": gen_s,
                        "l2": "inputs (%.1f GB) larger than L2; no flush needed" % (8 * E / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "edge phase (%s)" % args.schedule,
-                         "avg_launch_ms": avg_edge_ms, "alg_bytes_per_launch": alg_edge,
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "traffic_note": traffic_note, "kernel": kernel, "avg_launch_ms": avg_top_ms,
+                         "alg_bytes_per_launch": alg_top,
+                         "edge_phase": {"ms_per_iteration": avg_edge_ms, "alg_bytes": alg_edge,
+                                        "achieved": edge_achieved, "frac": edge_achieved / peak},
                          "iteration_frac": iter_achieved / peak},
             "gpu_launches": launches,
             "clocks": clk.summary()}

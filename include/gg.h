@@ -102,6 +102,9 @@ typedef struct {
   int64_t gpu_launches; /* kernels this call launched */
   double edge_ms;       /* device time of the edge-traversal phase (events)  */
   int64_t edge_launches;/* number of edge-traversal phases timed in edge_ms */
+  double top_ms;        /* device time of the call's dominant kernel (events; 0 if none) */
+  int64_t top_launches; /* launches of that kernel timed in top_ms */
+  int64_t top_edges;    /* edges one launch of it processes */
 } gg_stats;
 
 typedef struct {

@@ -56,7 +56,8 @@ class GGStats(C.Structure):
                 ("direction_log_cap", C.c_int64), ("direction_log_len", C.c_int64),
                 ("kernel_ms", C.c_double), ("wall_ms", C.c_double),
                 ("gpu_launches", C.c_int64), ("edge_ms", C.c_double),
-                ("edge_launches", C.c_int64)]
+                ("edge_launches", C.c_int64), ("top_ms", C.c_double),
+                ("top_launches", C.c_int64), ("top_edges", C.c_int64)]
 
 
 class GGDeviceInfo(C.Structure):

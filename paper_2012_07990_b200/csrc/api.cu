@@ -102,6 +102,8 @@ static void fill_stats(Runtime& rt, gg_stats* out, double wall_ms, double kernel
   out->kernel_ms = kernel_ms;
   out->gpu_launches = launches;
   out->edge_ms = rt.edge_ms(&out->edge_launches);
+  out->top_ms = rt.top_ms(&out->top_launches);
+  out->top_edges = rt.top_edges;
 }
 
 // Times a driver call: CUDA events around the device work, wall clock around all.

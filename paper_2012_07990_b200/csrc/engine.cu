@@ -213,6 +213,10 @@ Runtime::~Runtime() {
     cudaEventDestroy(p.second);
   }
   if (edge_open) cudaEventDestroy(edge_open);
+  for (auto& p : top_events) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
 }
 
 void Runtime::edge_begin() {
@@ -237,6 +241,18 @@ double Runtime::edge_ms(int64_t* launches) {
     total += ms;
   }
   if (launches) *launches = (int64_t)edge_events.size();
+  return total;
+}
+
+double Runtime::top_ms(int64_t* launches) {
+  double total = 0;
+  for (auto& p : top_events) {
+    GG_CUDA(cudaEventSynchronize(p.second));
+    float ms = 0;
+    GG_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+    total += ms;
+  }
+  if (launches) *launches = (int64_t)top_events.size();
   return total;
 }
 

@@ -69,6 +69,12 @@ struct Runtime {
   void edge_begin();
   void edge_end();
   double edge_ms(int64_t* launches);   // syncs; sums all recorded phases
+  // the call's dominant kernel (PageRank EB: the hot-segment gather), timed
+  // the same way; top_edges = edges one launch processes
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> top_events;
+  int64_t top_edges = 0;
+  void top_record(cudaEvent_t a, cudaEvent_t b) { top_events.emplace_back(a, b); }
+  double top_ms(int64_t* launches);
 
   Runtime(const Graph* graph, const gg_exec* c);
   ~Runtime();

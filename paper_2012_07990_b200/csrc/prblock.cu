@@ -660,12 +660,20 @@ struct PrRank {
   CT* cur(int64_t it) const { return (it & 1) ? c1 : c0; }
   CT* nxt(int64_t it) const { return (it & 1) ? c0 : c1; }
   // Alg. 2: segments in order, cold first, the hot one last
+  Runtime* rt_top = nullptr;  // records the hot-segment launches (dominant kernel)
   void edges(int64_t it, cudaStream_t st) {
     const CT* c = cur(it);
     for (int64_t k = 1; k <= L->K; ++k) {
       const int64_t sg = k == L->K ? 0 : k;
       const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
       if (e1 <= e0) continue;
+      cudaEvent_t ta = nullptr, tb = nullptr;
+      if (sg == 0 && rt_top) {
+        GG_CUDA(cudaEventCreate(&ta));
+        GG_CUDA(cudaEventCreate(&tb));
+        GG_CUDA(cudaEventRecord(ta, st));
+        rt_top->top_edges = e1 - e0;
+      }
       if (sg == 0 && hc.nhot > 0 && hc.per_sm == 2)
         k_pr_edges_hot<CT, 512, 2><<<hc.hot_grid, 512, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, c,
                                                                                   acc, hc.nhot);
@@ -676,6 +684,10 @@ struct PrRank {
         k_pr_edges<CT, true><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
       else
         k_pr_edges<CT, false><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+      if (ta) {
+        GG_CUDA(cudaEventRecord(tb, st));
+        rt_top->top_record(ta, tb);
+      }
       ++launches;
     }
     GG_LAUNCH_CHECK();
@@ -709,6 +721,7 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   std::lock_guard<std::mutex> wlk(L->w_mu);
   PrRank<CT> R;
   R.bind(L, dev, iters_cap);
+  R.rt_top = &rt;
   R.init(iters_cap, st);
   int64_t it = 0;
   if (!fusion) {
@@ -876,6 +889,7 @@ int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r
   std::lock_guard<std::mutex> wlk(L->w_mu);
   PrRank<CT> R;
   R.bind(L, g.dev, iters_cap);
+  R.rt_top = &rt;
   R.init(iters_cap, rt.stream);
   std::vector<PrRank<CT>*> rp{&R};
   int64_t it = pagerank_blocked_ranks<CT>(rp, ex, max_iters, tol, damping, s.direction, rt.stream, rt);

@@ -72,6 +72,9 @@ class RunStats:
     gpu_launches: int = 0
     edge_ms: float = 0.0
     edge_launches: int = 0
+    top_ms: float = 0.0       # dominant kernel (PageRank EB: hot-segment gather)
+    top_launches: int = 0
+    top_edges: int = 0        # edges per launch of it
 
     def to_dict(self):
         return asdict(self)
@@ -83,7 +86,7 @@ class RunStats:
         return cls(st.dispatch_count, st.rounds, st.edges_traversed, log,
                    st.frontier_conversions, st.frontier_allocations, st.reused_frontiers,
                    st.creation_passes, st.kernel_ms, st.wall_ms, st.gpu_launches,
-                   st.edge_ms, st.edge_launches)
+                   st.edge_ms, st.edge_launches, st.top_ms, st.top_launches, st.top_edges)
 
 
 class Runtime:
