@@ -210,6 +210,22 @@ def rmat12_cases():
         json.dump(out, fh)
 
 
+def tune_candidates():
+    """tests/golden/tune_candidates.json: the reference tuner's candidate
+    lists (cli.candidate_schedules) per algorithm -- count, first five keys,
+    and a seeded random strategy with a limit."""
+    import json
+    from schedge import cli, sched
+    out = {}
+    for algo in cli.ALGO_DIMENSIONS:
+        c = cli.candidate_schedules(algo)
+        r = cli.candidate_schedules(algo, seed=3, strategy="random", limit=7)
+        out[algo] = {"n": len(c), "first5": [sched.schedule_key(s) for s in c[:5]],
+                     "random3_7": [sched.schedule_key(s) for s in r]}
+    with open(os.path.join(OUT, "tune_candidates.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     t = time.time()
@@ -221,3 +237,4 @@ if __name__ == "__main__":
     rmat12_cases()
     print("rmat12: %.1fs" % (time.time() - t))
     print("c1:", c1_pagerank())
+    tune_candidates()

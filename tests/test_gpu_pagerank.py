@@ -118,3 +118,35 @@ def test_pagerank_errors(gg):
         gg.pagerank(g, gg.ScheduleProgram({"s0:s1": gg.HybridSchedule()}))
     with pytest.raises(gg.ScheduleError, match="not exposed"):
         gg.pagerank(g, gg.ScheduleProgram({"nope": gg.Schedule()}))
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_pagerank_edge_blocking_dominant_kernel_stats(gg, fp32):
+    """The EB run times its hot-segment kernel (RunStats.top_*), which the
+    bench's roofline uses: one launch per iteration, hot edges <= E."""
+    V, s, d = gen.rmat(14, 16, seed=3)
+    g = gg.Graph.from_coo(V, s, d)
+    sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True)
+    r = gg.pagerank(g, program_with(sch), max_iters=10, tolerance=0.0, contrib_fp32=fp32)
+    want, _ = oracle.pagerank(V, s, d, 10, 0.0)
+    assert max_rel_err(r.values, want) < PR_TOL
+    st = r.stats
+    assert st.top_launches == 10 and st.top_ms > 0.0
+    assert 0 < st.top_edges <= len(s)
+    assert st.edge_launches == 10 and st.edge_ms >= st.top_ms
+
+
+def test_pagerank_edge_blocking_hub_source_beyond_smem_cache(gg):
+    """Sources ranked past the shared-memory hot cache (a star whose centre
+    is the only source, plus thousands of low-degree sources) gather from
+    global memory inside the hot kernel."""
+    rng = np.random.default_rng(5)
+    V = 200000
+    s = np.concatenate([np.zeros(50000, np.int64), rng.integers(1, V, 400000)])
+    d = rng.integers(0, V, len(s))
+    g = gg.Graph.from_coo(V, s, d)
+    want, _ = oracle.pagerank(V, s, d, 15, 0.0)
+    for fp32 in (False, True):
+        sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True)
+        r = gg.pagerank(g, program_with(sch), max_iters=15, tolerance=0.0, contrib_fp32=fp32)
+        assert max_rel_err(r.array, want) < PR_TOL
