@@ -169,6 +169,14 @@ int64_t gg_default_blocking_size(const gg_graph* g);
 /* Alg. 1 on the device (blocking.py:78-113): stable partition of the COO by
  * dst / n.  Cached on the graph per n (blocking.py:69-75). */
 int gg_block_edges(gg_graph* g, int64_t n, gg_blocked** out, double* prep_ms);
+/* Install a layout read from a blocked-graph sidecar (blocking.load_blocked,
+ * blocking.py:200-217) instead of recomputing Alg. 1: host (or device)
+ * arrays, inclusive segment ends; validated against the graph (segment
+ * bounds, every edge in its segment, same edge multiset) and cached as
+ * gg_block_edges(g, n) would have cached it. */
+int gg_blocked_install(gg_graph* g, int64_t n, int64_t num_segments, const int64_t* segment_start,
+                       const int32_t* src, const int32_t* dst, const uint32_t* weights,
+                       gg_blocked** out);
 int gg_blocked_info(const gg_blocked* b, int64_t* num_segments, int64_t* n);
 /* which: 0 segment_start(int64,S) 1 src(int32,E) 2 dst(int32,E) 3 weight(uint32,E) */
 int gg_blocked_copy_array(const gg_blocked* b, int32_t which, void* out);

@@ -93,6 +93,7 @@ SIGNATURES = {
     "gg_block_edges": (I32, [VP, I64, PP, C.POINTER(F64)]),
     "gg_blocked_info": (I32, [VP, C.POINTER(I64), C.POINTER(I64)]),
     "gg_blocked_copy_array": (I32, [VP, I32, VP]),
+    "gg_blocked_install": (I32, [VP, I64, I64, VP, VP, VP, VP, PP]),
     "gg_runtime_create": (I32, [VP, C.POINTER(GGExec), PP]),
     "gg_runtime_destroy": (I32, [VP]),
     "gg_runtime_stats": (I32, [VP, C.POINTER(GGStats)]),

@@ -121,3 +121,39 @@ def load_blocked(path):
         dst = np.fromfile(fh, dtype="<i8", count=ne).tolist()
         w = np.fromfile(fh, dtype="<i8", count=ne).tolist() if has_w else None
     return BlockedGraph(nv, n, seg, src, dst, w)
+
+
+def load_blocked_to_device(path, g=None, device=0, symmetric=False):
+    """A sidecar straight to the device: the layout is
+    installed as the graph's cached Alg. 1 result for its width, validated
+    against the graph (segment bounds, edge multiset), without re-blocking.
+    With ``g`` None the graph itself is built from the sidecar's edges (the
+    blocked order is a valid COO order, and Alg. 1 is stable, so blocking it
+    again would reproduce the same layout).  Returns the device Graph."""
+    from .graphio import Graph, GraphLoadError
+    with open(path, "rb") as fh:
+        if fh.read(len(_SIDECAR_MAGIC)) != _SIDECAR_MAGIC:
+            raise EngineError("%s: not a blocked-graph sidecar" % path)
+        version, nv, ne, n, ns, has_w = struct.unpack("<qqqqqq", fh.read(48))
+        if version != _SIDECAR_VERSION:
+            raise EngineError("%s: unsupported sidecar version %d" % (path, version))
+        seg = np.fromfile(fh, dtype="<i8", count=ns)
+        src = np.fromfile(fh, dtype="<i8", count=ne)
+        dst = np.fromfile(fh, dtype="<i8", count=ne)
+        w = np.fromfile(fh, dtype="<i8", count=ne) if has_w else None
+    if len(seg) != ns or len(src) != ne or len(dst) != ne or (has_w and len(w) != ne):
+        raise EngineError("%s: truncated sidecar" % path)
+    if ne and (max(src.max(), dst.max()) >= min(nv, 2 ** 31) or min(src.min(), dst.min()) < 0):
+        raise GraphLoadError("%s: vertex id out of range" % path)
+    s32 = np.ascontiguousarray(src.astype(np.int32))
+    d32 = np.ascontiguousarray(dst.astype(np.int32))
+    w32 = None if w is None else np.ascontiguousarray(w.astype(np.uint32))
+    if g is None:
+        g = Graph.from_coo(nv, s32, d32, w32, symmetric=symmetric, device=device)
+    elif g.num_vertices != nv or g.num_edges != ne:
+        raise EngineError("%s: sidecar does not match the graph (%d/%d vertices, %d/%d edges)"
+                          % (path, nv, g.num_vertices, ne, g.num_edges))
+    seg = np.ascontiguousarray(seg.astype(np.int64))
+    _lib.call("gg_blocked_install", g.handle, int(n), int(ns), _lib.ptr(seg), _lib.ptr(s32),
+              _lib.ptr(d32), _lib.ptr(w32), None)
+    return g

@@ -287,6 +287,17 @@ int gg_block_edges(gg_graph* g, int64_t n, gg_blocked** out, double* prep_ms) {
   GG_API_END
 }
 
+int gg_blocked_install(gg_graph* g, int64_t n, int64_t num_segments, const int64_t* segment_start,
+                       const int32_t* src, const int32_t* dst, const uint32_t* weights, gg_blocked** out) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(segment_start);
+  if (g->g->E > 0) { NEED(src); NEED(dst); }
+  Blocked* b = blocked_install(*g->g, n, num_segments, segment_start, src, dst, weights);
+  if (out) *out = new gg_blocked{b};
+  GG_API_END
+}
+
 int gg_blocked_info(const gg_blocked* b, int64_t* nseg, int64_t* n) {
   GG_API_BEGIN
   NEED(b);

@@ -491,6 +491,80 @@ int64_t default_blocking_size(const Graph& g) {
   return n < g.V ? n : (g.V > 0 ? g.V : 1);
 }
 
+// Sidecar install (blocking.load_blocked, blocking.py:200-217, straight to the
+// device): validates the layout against the graph -- segment ends, every
+// edge inside its segment, and the edge multiset (order-free hash sum) --
+// then caches it as blocked_for(g, n) would have built it.
+__global__ void k_seg_check(const int32_t* dst, const int64_t* seg_end, int64_t nseg, int64_t E, int64_t n,
+                            int* bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = dst[e] / n;
+    const int64_t lo = s ? seg_end[s - 1] : 0;
+    if (s >= nseg || e < lo || e >= seg_end[s]) *bad = 1;
+  }
+}
+__global__ void k_edge_hash(const int32_t* src, const int32_t* dst, const uint32_t* w, int64_t E,
+                            unsigned long long* h) {
+  unsigned long long acc = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    acc += mix64(((uint64_t)(uint32_t)src[e] << 32) ^ (uint32_t)dst[e] ^ ((uint64_t)(w ? w[e] : 0u) << 17));
+  acc = warp_sum(acc);
+  if (lane_id() == 0) atomicAdd(h, acc);
+}
+
+Blocked* blocked_install(Graph& g, int64_t n, int64_t nseg, const int64_t* seg_end, const int32_t* src,
+                         const int32_t* dst, const uint32_t* w) {
+  if (n < 1) fail(GG_ERR_VALUE, "vertices per segment must be >= 1");
+  if (g.V == 0) fail(GG_ERR_VALUE, "empty graph");
+  if (!g.has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
+  if (nseg != (g.V + n - 1) / n) fail(GG_ERR_VALUE, "sidecar segment count does not match the graph");
+  if ((w != nullptr) != g.weighted) fail(GG_ERR_VALUE, "sidecar weights do not match the graph");
+  for (int64_t s = 0; s < nseg; ++s)
+    if (seg_end[s] < (s ? seg_end[s - 1] : 0) || seg_end[s] > g.E)
+      fail(GG_ERR_VALUE, "sidecar segment ends are not monotone");
+  if (nseg && seg_end[nseg - 1] != g.E) fail(GG_ERR_VALUE, "sidecar edge count does not match the graph");
+  DeviceGuard guard(g.dev);
+  double t0 = now_ms();
+  auto b = std::make_unique<Blocked>();
+  b->n = n;
+  b->E = g.E;
+  b->nseg = nseg;
+  b->seg_end.alloc(nseg);
+  b->src.alloc(g.E);
+  b->dst.alloc(g.E);
+  GG_CUDA(cudaMemcpy(b->seg_end.p, seg_end, nseg * 8, cudaMemcpyDefault));
+  GG_CUDA(cudaMemcpy(b->src.p, src, g.E * 4, cudaMemcpyDefault));
+  GG_CUDA(cudaMemcpy(b->dst.p, dst, g.E * 4, cudaMemcpyDefault));
+  if (w) {
+    b->w.alloc(g.E);
+    GG_CUDA(cudaMemcpy(b->w.p, w, g.E * 4, cudaMemcpyDefault));
+  }
+  DevBuf<int> bad(1);
+  bad.zero();
+  DevBuf<unsigned long long> h(2);
+  h.zero();
+  if (g.E) {
+    k_check_range<<<grid_for(g.E, 256, g.dev), 256>>>(b->src.p, g.E, g.V, bad.p);
+    k_check_range<<<grid_for(g.E, 256, g.dev), 256>>>(b->dst.p, g.E, g.V, bad.p);
+    k_seg_check<<<grid_for(g.E, 256, g.dev), 256>>>(b->dst.p, b->seg_end.p, nseg, g.E, n, bad.p);
+    k_edge_hash<<<grid_for(g.E, 256, g.dev), 256>>>(b->src.p, b->dst.p, w ? b->w.p : nullptr, g.E, h.p);
+    k_edge_hash<<<grid_for(g.E, 256, g.dev), 256>>>(g.coo_src.p, g.coo_dst.p, g.weighted ? g.coo_w.p : nullptr,
+                                                    g.E, h.p + 1);
+    GG_LAUNCH_CHECK();
+  }
+  int hb = 0;
+  unsigned long long hh[2];
+  GG_CUDA(cudaMemcpy(&hb, bad.p, 4, cudaMemcpyDeviceToHost));
+  GG_CUDA(cudaMemcpy(hh, h.p, 16, cudaMemcpyDeviceToHost));
+  if (hb) fail(GG_ERR_VALUE, "sidecar edges are out of range or outside their segments");
+  if (hh[0] != hh[1]) fail(GG_ERR_VALUE, "sidecar edges are not the graph's edges");
+  b->prep_ms = now_ms() - t0;
+  std::lock_guard<std::mutex> lk(g.mu);
+  Blocked* raw = b.get();
+  g.blocked[n] = std::move(b);
+  return raw;
+}
+
 Blocked* blocked_for(Graph& g, int64_t n) {
   if (n < 1) fail(GG_ERR_VALUE, "vertices per segment must be >= 1");
   if (g.V == 0) fail(GG_ERR_VALUE, "empty graph");

@@ -62,6 +62,8 @@ std::unique_ptr<Graph> generate_graph(int dev, int kind, int scale, int edge_fac
                                       double b, double c, uint64_t seed, int flags);
 
 Blocked* blocked_for(Graph& g, int64_t n);  // blocking.blocked_for (blocking.py:69-75)
+Blocked* blocked_install(Graph& g, int64_t n, int64_t nseg, const int64_t* seg_end, const int32_t* src,
+                         const int32_t* dst, const uint32_t* w);
 int64_t default_blocking_size(const Graph& g);
 
 // Stable sort helper: returns the permutation that stably sorts `keys`

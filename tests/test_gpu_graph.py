@@ -69,3 +69,36 @@ def test_block_edges_matches_reference(gg, golden_small):
         bg = gg.block_edges(g, case["n"])
         assert bg.segment_start == case["segment_start"]
         assert bg.edges_src == case["src"] and bg.edges_dst == case["dst"]
+
+
+def test_sidecar_straight_to_device(tmp_path):
+    """convert -> sidecar -> install on the device (no Alg. 1 rerun); the
+    installed layout equals block_edges' and drives an EDGE_ONLY+BLOCKED run;
+    a tampered sidecar is rejected."""
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.blocking import block_edges, load_blocked_to_device, save_blocked
+    from paper_2012_07990_b200.engine import binding_pod  # noqa: F401
+    g = gg.generate_rmat(10, 8, seed=9, weights=True)
+    bg = block_edges(g, 100)
+    path = str(tmp_path / "g.blk")
+    save_blocked(bg, path)
+    g2 = gg.Graph.from_coo(g.num_vertices, g.coo_src, g.coo_dst, g.coo_weights)
+    load_blocked_to_device(path, g2)
+    bg2 = block_edges(g2, 100)  # cached: the installed layout
+    assert bg2.segment_start == bg.segment_start and bg2.edges_src == bg.edges_src
+    assert bg2.edges_dst == bg.edges_dst and bg2.edges_weight == bg.edges_weight
+    g3 = load_blocked_to_device(path)  # graph from the sidecar itself
+    assert g3.num_edges == g.num_edges
+    prog = gg.ScheduleProgram({"s0:s1": gg.Schedule(load_balance="EDGE_ONLY", blocking=True,
+                                                    blocking_size=100)})
+    want = gg.bfs_levels(gg.bfs(g, 0, prog).values)
+    assert gg.bfs_levels(gg.bfs(g3, 0, prog).values) == want
+    # tamper: move one edge into the wrong segment
+    import numpy as np
+    bad = np.fromfile(path, dtype=np.uint8).copy()
+    off = 8 + 48 + 8 * len(bg.segment_start) + 8 * g.num_edges  # start of dst array
+    bad[off:off + 8] = np.frombuffer(np.int64(g.num_vertices - 1).tobytes(), np.uint8)
+    bad.tofile(str(tmp_path / "bad.blk"))
+    g4 = gg.Graph.from_coo(g.num_vertices, g.coo_src, g.coo_dst, g.coo_weights)
+    with pytest.raises(ValueError):
+        load_blocked_to_device(str(tmp_path / "bad.blk"), g4)
