@@ -360,7 +360,30 @@ __device__ __forceinline__ void pr_load_edges(const int32_t* __restrict__ src, c
 // warp segmented scan per step; each destination run issues one f64 add.
 // kSmem: sources < nhot are read from the CTA's shared-memory copy of the
 // hottest contributions (degree-renumbered ids: hot = small).
-template <class CT, bool kSmem>
+// Gather flavours for the hot kernel (GG_PR_GATHER): 0 ld.global.nc (default),
+// 1 ld.global.cg (L2 only), 2 ld.global.nc.L1::no_allocate.
+template <int kLoad>
+__device__ __forceinline__ double ld_gather(const double* p) {
+  if (kLoad == 1) return __ldcg(p);
+  if (kLoad == 2) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  }
+  return __ldg(p);
+}
+template <int kLoad>
+__device__ __forceinline__ float ld_gather(const float* p) {
+  if (kLoad == 1) return __ldcg(p);
+  if (kLoad == 2) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+  }
+  return __ldg(p);
+}
+
+template <class CT, bool kSmem, int kLoad = 0>
 __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const int32_t (&dv)[kE], const CT* contrib,
                                                double* acc, int coherent, const CT* s_hot, int32_t nhot) {
   const int lane = lane_id();
@@ -370,7 +393,7 @@ __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const in
     if (kSmem)
       v[q] = dv[q] < 0 ? 0.0
              : su[q] < nhot ? (double)s_hot[su[q]]
-             : (double)__ldg(contrib + su[q]);
+             : (double)ld_gather<kLoad>(contrib + su[q]);
     else
       v[q] = dv[q] < 0 ? 0.0 : (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q]));
   }
@@ -419,7 +442,7 @@ __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const in
 // segment: warps stride over kE*32-edge steps; the next step's edges are
 // loaded (registers) before the current step's gathers, so the DRAM latency
 // of the edge stream overlaps the L2 latency of the gathers.
-template <class CT, bool kSmem = false, bool kPrefetch = true>
+template <class CT, bool kSmem = false, bool kPrefetch = true, int kLoad = 0>
 __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                              int64_t e0, int64_t e1, const CT* contrib, double* acc,
                                              int coherent, const CT* s_hot = nullptr, int32_t nhot = 0) {
@@ -435,12 +458,12 @@ __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, co
   for (; base < e1; base += stride) {
     if (!kPrefetch) {
       if (base != start + warp * 32 * kE) pr_load_edges(src, dst, base + lane * kE, e0, e1, su, dv);
-      pr_reduce_step<CT, kSmem>(su, dv, contrib, acc, coherent, s_hot, nhot);
+      pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot);
       continue;
     }
     int32_t nsu[kE], ndv[kE];
     pr_load_edges(src, dst, base + stride + lane * kE, e0, e1, nsu, ndv);  // dead past e1
-    pr_reduce_step<CT, kSmem>(su, dv, contrib, acc, coherent, s_hot, nhot);
+    pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot);
 #pragma unroll
     for (int q = 0; q < kE; ++q) {
       su[q] = nsu[q];
@@ -459,7 +482,7 @@ static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, con
 // are staged once per CTA in shared memory; their gathers leave the L1TEX
 // line pipeline and the L2 (the two bounds of this kernel, ~1 line/clk/SM)
 // for the shared-memory banks.
-template <class CT, int kThreads, int kMinBlocks>
+template <class CT, int kThreads, int kMinBlocks, int kLoad = 0>
 static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(const int32_t* src, const int32_t* dst,
                                                                              int64_t e0, int64_t e1, const CT* contrib,
                                                                              double* acc, int32_t nhot) {
@@ -470,7 +493,7 @@ static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(co
     reinterpret_cast<int4*>(s_raw)[i] = __ldg(reinterpret_cast<const int4*>(contrib) + i);
   for (int i = n4 * (16 / (int)sizeof(CT)) + threadIdx.x; i < nhot; i += blockDim.x) s_hot[i] = __ldg(contrib + i);
   __syncthreads();
-  pr_edges_seg<CT, true>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
+  pr_edges_seg<CT, true, true, kLoad>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
 }
 
 // vertex pass: rank' = base + d*acc, L1, next dangling mass, next contrib, acc reset.
@@ -579,6 +602,7 @@ struct HotCfg {
   int32_t nhot = 0;
   int per_sm = 1;
   bool prefetch = true;
+  int gather = 0;
   unsigned grid = 0, hot_grid = 0;
 };
 
@@ -612,6 +636,11 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
   }
   const char* pf_env = getenv("GG_PR_PREFETCH");
   h.prefetch = !(pf_env && atoi(pf_env) == 0);
+  if (const char* ge = getenv("GG_PR_GATHER")) h.gather = std::max(0, std::min(2, atoi(ge)));
+  if (h.nhot && h.per_sm == 1 && h.gather) {
+    const void* fn = h.gather == 1 ? (const void*)k_pr_edges_hot<CT, 1024, 1, 1> : (const void*)k_pr_edges_hot<CT, 1024, 1, 2>;
+    GG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
+  }
   h.grid = (unsigned)sm_count(dev) * 8;
   h.hot_grid = (unsigned)sm_count(dev) * h.per_sm;
   return h;
@@ -677,6 +706,12 @@ struct PrRank {
       if (sg == 0 && hc.nhot > 0 && hc.per_sm == 2)
         k_pr_edges_hot<CT, 512, 2><<<hc.hot_grid, 512, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1, c,
                                                                                   acc, hc.nhot);
+      else if (sg == 0 && hc.nhot > 0 && hc.gather == 1)
+        k_pr_edges_hot<CT, 1024, 1, 1><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
+                                                                                       e1, c, acc, hc.nhot);
+      else if (sg == 0 && hc.nhot > 0 && hc.gather == 2)
+        k_pr_edges_hot<CT, 1024, 1, 2><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
+                                                                                       e1, c, acc, hc.nhot);
       else if (sg == 0 && hc.nhot > 0)
         k_pr_edges_hot<CT, 1024, 1><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1,
                                                                                     c, acc, hc.nhot);
