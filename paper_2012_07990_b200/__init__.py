@@ -10,7 +10,8 @@ from .sched import (HybridSchedule, ParseError, Schedule, ScheduleError, Schedul
 from .runtime import EdgeContext, EngineError, ExecConfig, RunStats, Runtime
 from .frontier import BITMAP, BOOLMAP, SPARSE, FrontierError, VertexSubset
 from .graphio import (Graph, GraphLoadError, generate_grid, generate_kronecker, generate_rmat,
-                      load_edge_list, load_graph, out_degree, with_random_weights)
+                      load_edge_list, load_graph, load_matrix_market, out_degree,
+                      with_random_weights)
 from .priority import UNREACHED
 from .blocking import BlockedGraph, block_edges, default_blocking_size
 from .engine import edgeset_apply, fused_loop, hybrid_apply
@@ -24,7 +25,7 @@ __all__ = [
     "ALGO_LABELS", "ALGO_NAMES", "AlgoResult", "bc", "bfs", "bfs_levels", "cc_soman",
     "pagerank", "sssp_delta", "BlockedGraph", "block_edges", "default_blocking_size",
     "BITMAP", "BOOLMAP", "SPARSE", "VertexSubset", "FrontierError", "Graph", "GraphLoadError",
-    "load_edge_list", "load_graph", "out_degree", "with_random_weights", "generate_rmat",
+    "load_edge_list", "load_graph", "load_matrix_market", "out_degree", "with_random_weights", "generate_rmat",
     "generate_grid", "generate_kronecker", "UNREACHED", "EdgeContext", "EngineError",
     "ExecConfig", "RunStats", "Runtime", "HybridSchedule", "ParseError", "Schedule",
     "ScheduleError", "ScheduleProgram", "enumerate_space", "parse_schedule", "pretty_print",

@@ -224,7 +224,75 @@ def load_edge_list(path, weighted=False, symmetrize=False, device=0):
                           device=device)
 
 
+def load_matrix_market(path, weighted=False, device=0):
+    """MatrixMarket coordinate file (graphio.py:193-261): 1-based ids, a
+    'symmetric' banner mirrors every off-diagonal entry, integer values as
+    weights; the declared dimensions bound the ids."""
+    with open(path) as fh:
+        banner = fh.readline()
+        if not banner.startswith("%%MatrixMarket matrix coordinate"):
+            raise GraphLoadError("%s: not a MatrixMarket coordinate file" % path)
+        tok = banner.strip().lower().split()
+        fld = tok[3] if len(tok) > 3 else "pattern"
+        symmetric = len(tok) > 4 and tok[4] == "symmetric"
+        if weighted and fld == "pattern":
+            raise GraphLoadError("%s: pattern matrix has no weights" % path)
+        lineno, dims = 1, None
+        src, dst, wts = [], [], ([] if weighted else None)
+        for raw in fh:
+            lineno += 1
+            line = raw.strip()
+            if not line or line[0] == "%":
+                continue
+            parts = line.split()
+            if dims is None:
+                if len(parts) != 3:
+                    raise GraphLoadError("%s:%d: bad size line %r" % (path, lineno, line))
+                dims = [int(x) for x in parts]
+                if dims[0] != dims[1]:
+                    raise GraphLoadError("%s: adjacency matrix must be square" % path)
+                continue
+            if len(parts) < 2:
+                raise GraphLoadError("%s:%d: malformed entry %r" % (path, lineno, line))
+            i, j = int(parts[0]) - 1, int(parts[1]) - 1
+            if i < 0 or j < 0:
+                raise GraphLoadError("%s:%d: ids are 1-based" % (path, lineno))
+            if weighted:
+                if len(parts) < 3:
+                    raise GraphLoadError("%s:%d: missing value token" % (path, lineno))
+                val = float(parts[2])
+                if val != int(val) or val < 0:
+                    raise GraphLoadError("%s:%d: weights must be non-negative integers"
+                                         % (path, lineno))
+            pairs = [(i, j)] + ([(j, i)] if symmetric and i != j else [])
+            for a, b in pairs:
+                src.append(a)
+                dst.append(b)
+                if weighted:
+                    wts.append(int(val))
+    if dims is None:
+        raise GraphLoadError("%s: missing size line" % path)
+    if not src:
+        raise GraphLoadError("%s: no edges" % path)
+    n = dims[0]
+    if max(max(src), max(dst)) >= n:
+        raise GraphLoadError("%s: entry outside declared dimensions" % path)
+    return Graph.from_coo(n, src, dst, wts, symmetric=symmetric,
+                          diagnostics={"declared_nnz": dims[2]}, device=device)
+
+
 def load_graph(path, weighted=False, symmetrize=False, device=0):
+    """MatrixMarket banner or plain edge list (graphio.py:264-278)."""
+    with open(path) as fh:
+        first = fh.readline()
+    if first.startswith("%%MatrixMarket"):
+        g = load_matrix_market(path, weighted=weighted, device=device)
+        if symmetrize and not g.symmetric:
+            s, d, w, dropped = symmetrize_coo(g.coo_src, g.coo_dst, g.coo_weights)
+            g = Graph.from_coo(g.num_vertices, s, d, w, symmetric=True,
+                               diagnostics=dict(g.diagnostics, duplicates_collapsed=dropped),
+                               device=device)
+        return g
     return load_edge_list(path, weighted=weighted, symmetrize=symmetrize, device=device)
 
 
