@@ -210,6 +210,34 @@ def rmat12_cases():
         json.dump(out, fh)
 
 
+def scale16_cases():
+    """Larger pins (reference at scale <= 18): BFS levels and CC
+    labels on symmetrised RMAT-16 (seed 2), delta-stepping distances on the
+    128x128 grid (weights seed 4), BC on symmetrised RMAT-13 (seed 6)."""
+    V, s, d = gen.rmat(16, 16, seed=2)
+    ss, dd, _, _ = _symmetrize(s.tolist(), d.tolist(), None)
+    gs = Graph.from_coo(V, ss, dd, symmetric=True)
+    hub = int(np.argmax(np.diff(np.asarray(gs.out_offsets))))
+    levels = algos.bfs_levels(algos.bfs(gs, hub).values)
+    labels = algos.cc_soman(gs).values
+    Vg, gsrc, gdst = gen.grid(128)
+    wg = gen.weights(len(gsrc), 4)
+    gg_ = Graph.from_coo(Vg, gsrc.tolist(), gdst.tolist(), wg.tolist())
+    dist = {}
+    for delta in (64, 1024):
+        r = algos.sssp_delta(gg_, 0, program_with(Schedule(delta=delta)))
+        dist[delta] = np.asarray([-1 if math.isinf(x) else int(x) for x in r.values], np.int64)
+    Vb, bs, bd = gen.rmat(13, 8, seed=6)
+    bss, bdd, _, _ = _symmetrize(bs.tolist(), bd.tolist(), None)
+    gb = Graph.from_coo(Vb, bss, bdd, symmetric=True)
+    bsrc = [int(np.argmax(np.diff(np.asarray(gb.out_offsets)))), 5]
+    scores = np.asarray(algos.bc(gb, bsrc).values, np.float64)
+    np.savez_compressed(os.path.join(OUT, "scale16.npz"), bfs_source=hub,
+                        bfs_levels=np.asarray(levels, np.int32), cc_labels=np.asarray(labels, np.int32),
+                        sym_arcs=len(ss), sssp_d64=dist[64], sssp_d1024=dist[1024],
+                        bc_sources=np.asarray(bsrc), bc_scores=scores, bc_arcs=len(bss))
+
+
 def tune_candidates():
     """tests/golden/tune_candidates.json: the reference tuner's candidate
     lists (cli.candidate_schedules) per algorithm -- count, first five keys,
@@ -238,3 +266,4 @@ if __name__ == "__main__":
     print("rmat12: %.1fs" % (time.time() - t))
     print("c1:", c1_pagerank())
     tune_candidates()
+    scale16_cases()

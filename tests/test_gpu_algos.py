@@ -293,3 +293,52 @@ def test_etwc_hub_pass_bc(gg, hub_graph):
     prog = program_with(gg.Schedule(direction="PUSH", load_balance="ETWC"))
     srcs = [0, 150, 7]
     close_bc(gg.bc(g, srcs, prog).values, oracle.bc(g.num_vertices, off, nbr, srcs))
+
+
+# ---------------------------------------------------------------------------
+# scale-16 reference pins (tests/golden/scale16.npz)
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def s16():
+    import os
+    from tests.conftest import GOLDEN
+    return np.load(os.path.join(GOLDEN, "scale16.npz"))
+
+
+@pytest.mark.parametrize("sch", ["PUSH-ETWC", "PULL-VERTEX_BASED", "HYBRID", "PUSH-TWC"])
+def test_scale16_bfs_cc_vs_reference(gg, s16, sch):
+    g = gg.generate_rmat(16, 16, seed=2, symmetrize=True)
+    assert g.num_edges == int(s16["sym_arcs"])
+    if sch == "HYBRID":
+        s = gg.HybridSchedule(threshold=0.01, s1=gg.Schedule(direction="PUSH", load_balance="ETWC"),
+                              s2=gg.Schedule(direction="PULL", pull_frontier_repr="BITMAP",
+                                             frontier_creation="UNFUSED_BITMAP"))
+        prog = gg.ScheduleProgram({"s0:s1": s})
+    else:
+        d, lb = sch.split("-")
+        prog = program_with(gg.Schedule(direction=d, load_balance=lb))
+    for fusion in (False, True):
+        if fusion:
+            prog.bindings["s0"] = gg.Schedule(kernel_fusion=True)
+        r = gg.bfs(g, int(s16["bfs_source"]), prog)
+        assert np.array_equal(np.asarray(gg.bfs_levels(r.array)), s16["bfs_levels"])
+        if sch != "HYBRID":
+            assert np.array_equal(gg.cc_soman(g, prog).array, s16["cc_labels"])
+
+
+@pytest.mark.parametrize("lb", ["VERTEX_BASED", "ETWC", "WM"])
+def test_scale16_sssp_grid_vs_reference(gg, s16, lb):
+    g = gg.generate_grid(128, seed=4, weights=True)
+    for delta in (64, 1024):
+        for fusion in (False, True):
+            r = gg.sssp_delta(g, 0, program_with(gg.Schedule(load_balance=lb, delta=delta), fusion))
+            got = np.where(r.array == np.uint64(2**64 - 1), -1, r.array.astype(np.int64))
+            assert np.array_equal(got, s16["sssp_d%d" % delta]), (lb, delta, fusion)
+
+
+@pytest.mark.parametrize("lb", ["ETWC", "TWC", "VERTEX_BASED"])
+def test_scale16_bc_vs_reference(gg, s16, lb):
+    g = gg.generate_rmat(13, 8, seed=6, symmetrize=True)
+    assert g.num_edges == int(s16["bc_arcs"])
+    r = gg.bc(g, [int(x) for x in s16["bc_sources"]], program_with(gg.Schedule(load_balance=lb)))
+    close_bc(r.array, s16["bc_scores"])

@@ -118,3 +118,48 @@ def test_oracle_c1_pagerank_against_reference():
     ranks, it = oracle.pagerank(V, s, d, 20, 0.0)
     assert it == 20
     assert max_rel_err(ranks, z["ranks"]) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# scale-16 pins (tests/golden/scale16.npz, oracle/make_golden.py scale16_cases)
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def s16():
+    return np.load(os.path.join(GOLDEN, "scale16.npz"))
+
+
+def _sym(V, s, d):
+    from paper_2012_07990_b200.graphio import symmetrize_coo
+    ss, dd, _, _ = symmetrize_coo(s, d)
+    return ss.astype(np.int32), dd.astype(np.int32)
+
+
+def test_oracle_scale16_bfs_cc(s16):
+    V, s, d = gen.rmat(16, 16, seed=2)
+    ss, dd = _sym(V, s, d)
+    assert len(ss) == int(s16["sym_arcs"])
+    off, nbr, _ = _csr(V, ss, dd)
+    src = int(s16["bfs_source"])
+    assert np.array_equal(oracle.bfs_levels(V, off, nbr, src, parallel=True), s16["bfs_levels"])
+    labels, _ = oracle.cc(V, ss, dd)
+    assert np.array_equal(labels, s16["cc_labels"])
+
+
+def test_oracle_scale16_sssp_grid(s16):
+    V, s, d = gen.grid(128)
+    w = gen.weights(len(s), 4)
+    off, nbr, ww = _csr(V, s, d, w)
+    for delta in (64, 1024):
+        got, _ = oracle.sssp_delta(V, off, nbr, ww, 0, delta)
+        want = s16["sssp_d%d" % delta]
+        got = np.where(got == np.uint64(2**64 - 1), -1, got.astype(np.int64))
+        assert np.array_equal(got, want)
+
+
+def test_oracle_scale16_bc(s16):
+    V, s, d = gen.rmat(13, 8, seed=6)
+    ss, dd = _sym(V, s, d)
+    assert len(ss) == int(s16["bc_arcs"])
+    off, nbr, _ = _csr(V, ss, dd)
+    got = oracle.bc(V, off, nbr, [int(x) for x in s16["bc_sources"]])
+    assert max_rel_err(got[s16["bc_scores"] > 1e-6], s16["bc_scores"][s16["bc_scores"] > 1e-6]) < 1e-9
