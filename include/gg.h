@@ -280,10 +280,12 @@ int gg_bfs_virtual(const gg_graph* g, int32_t nparts, int64_t source, double thr
                    int32_t* parents, gg_stats* stats);
 /* Test mode of the partitioned run: `nparts` virtual ranks on the graph's
  * one device, each with its own layout and buffers, exchanging by copies in
- * the same order as the NCCL exchange.  EDGE_ONLY + BLOCKED only. */
+ * the same order as the NCCL exchange (fused_allgather = 0), or with the
+ * vertex pass storing into the other ranks' buffers as the multi-GPU fused
+ * all-gather does over NVLink (fused_allgather = 1).  EDGE_ONLY + BLOCKED. */
 int gg_pagerank_virtual(const gg_graph* g, int32_t nparts, const gg_binding* binding,
-                        int32_t fp32_contrib, int64_t max_iters, double tolerance, double damping,
-                        double* ranks, gg_stats* stats);
+                        int32_t fp32_contrib, int32_t fused_allgather, int64_t max_iters,
+                        double tolerance, double damping, double* ranks, gg_stats* stats);
 
 #ifdef __cplusplus
 }

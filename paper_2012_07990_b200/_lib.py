@@ -130,7 +130,7 @@ SIGNATURES = {
                                        C.POINTER(F64)]),
     "gg_bfs_dist": (I32, [VP, VP, I64, F64, VP, C.POINTER(GGStats)]),
     "gg_bfs_virtual": (I32, [VP, I32, I64, F64, VP, C.POINTER(GGStats)]),
-    "gg_pagerank_virtual": (I32, [VP, I32, C.POINTER(GGBinding), I32, I64, F64, F64, VP,
+    "gg_pagerank_virtual": (I32, [VP, I32, C.POINTER(GGBinding), I32, I32, I64, F64, F64, VP,
                                   C.POINTER(GGStats)]),
 }
 

@@ -632,7 +632,8 @@ int gg_bfs_virtual(const gg_graph* g, int32_t nparts, int64_t source, double thr
 }
 
 int gg_pagerank_virtual(const gg_graph* g, int32_t nparts, const gg_binding* binding, int32_t fp32_contrib,
-                        int64_t max_iters, double tolerance, double damping, double* ranks, gg_stats* stats) {
+                        int32_t fused_allgather, int64_t max_iters, double tolerance, double damping,
+                        double* ranks, gg_stats* stats) {
   GG_API_BEGIN
   NEED(g);
   NEED(binding);
@@ -645,9 +646,9 @@ int gg_pagerank_virtual(const gg_graph* g, int32_t nparts, const gg_binding* bin
   Runtime rt(g->g.get(), nullptr);
   CallTimer t(g->g->dev);
   if (fp32_contrib)
-    pagerank_blocked_virtual<float>(*g->g, s, nparts, max_iters, tolerance, damping, ranks, rt);
+    pagerank_blocked_virtual<float>(*g->g, s, nparts, max_iters, tolerance, damping, ranks, rt, fused_allgather != 0);
   else
-    pagerank_blocked_virtual<double>(*g->g, s, nparts, max_iters, tolerance, damping, ranks, rt);
+    pagerank_blocked_virtual<double>(*g->g, s, nparts, max_iters, tolerance, damping, ranks, rt, fused_allgather != 0);
   t.finish(g->g->dev, rt, stats);
   GG_API_END
 }

@@ -11,6 +11,7 @@
 // NCCL is resolved with dlopen at first use (reusing the libnccl.so.2 the
 // process already loaded, e.g. torch's), so libgg.so has no hard dependency.
 #include <dlfcn.h>
+#include <cstring>
 #include <nccl.h>
 #include "prpull.cuh"
 #include "prdist.cuh"
@@ -150,7 +151,84 @@ namespace gg {
 // of in-place broadcasts (one per owner).
 struct NcclExchange : PrExchange {
   gg_comm* c;
+  std::vector<void*> opened;  // IPC-mapped peer buffers (closed by unmap_peers)
   explicit NcclExchange(gg_comm* cc) : c(cc) {}
+  ~NcclExchange() override { unmap_peers(); }
+  // Fused all-gather over NVLink: every rank exports its two contribution
+  // buffers (cudaIpcGetMemHandle), the handles are all-gathered over NCCL,
+  // and each peer's buffers are mapped (cudaIpcOpenMemHandle).  Enabled by
+  // GG_PR_P2P=1 (all peers must report peer access); any failure leaves the
+  // NCCL all-gather in place.
+  bool map_peers(const std::vector<void*>& c0s, const std::vector<void*>& c1s, size_t bytes,
+                 std::vector<std::vector<void*>>& pc0, std::vector<std::vector<void*>>& pc1) override {
+    const char* e = getenv("GG_PR_P2P");
+    if (!e || atoi(e) == 0 || c->nranks < 2 || c->nranks - 1 > 15) return false;
+    // every rank must agree, so the decision itself is all-reduced (min);
+    // peer access is checked against the peers' actual device ordinals
+    int ok = 1;
+    {
+      DevBuf<int> devs(c->nranks);
+      GG_CUDA(cudaMemset(devs.p, 0xff, c->nranks * sizeof(int)));
+      GG_CUDA(cudaMemcpy(devs.p + c->rank, &c->dev, sizeof(int), cudaMemcpyHostToDevice));
+      NcclApi& api = nccl();
+      GG_NCCL(api.GroupStart());
+      for (int r = 0; r < c->nranks; ++r)
+        GG_NCCL(api.Broadcast(devs.p + r, devs.p + r, 1, ncclInt32, r, c->comm, 0));
+      GG_NCCL(api.GroupEnd());
+      std::vector<int> hd(c->nranks);
+      GG_CUDA(cudaMemcpy(hd.data(), devs.p, c->nranks * sizeof(int), cudaMemcpyDeviceToHost));
+      for (int r = 0; r < c->nranks; ++r) {
+        if (r == c->rank) continue;
+        int can = 0;
+        if (hd[r] == c->dev || cudaDeviceCanAccessPeer(&can, c->dev, hd[r]) != cudaSuccess) can = 0;
+        ok &= can;
+      }
+      cudaGetLastError();
+    }
+    cudaIpcMemHandle_t mine[2];
+    if (ok && (cudaIpcGetMemHandle(&mine[0], c0s[0]) != cudaSuccess ||
+               cudaIpcGetMemHandle(&mine[1], c1s[0]) != cudaSuccess)) ok = 0;
+    cudaGetLastError();
+    DevBuf<int> dok(1);
+    GG_CUDA(cudaMemcpy(dok.p, &ok, 4, cudaMemcpyHostToDevice));
+    GG_NCCL(nccl().AllReduce(dok.p, dok.p, 1, ncclInt32, ncclMin, c->comm, 0));
+    GG_CUDA(cudaMemcpy(&ok, dok.p, 4, cudaMemcpyDeviceToHost));
+    if (!ok) return false;
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    DevBuf<uint8_t> all(2 * hb * c->nranks);
+    GG_CUDA(cudaMemcpy(all.p + 2 * hb * c->rank, mine, 2 * hb, cudaMemcpyHostToDevice));
+    {
+      NcclApi& api = nccl();
+      GG_NCCL(api.GroupStart());
+      for (int r = 0; r < c->nranks; ++r)
+        GG_NCCL(api.Broadcast(all.p + 2 * hb * r, all.p + 2 * hb * r, 2 * hb, ncclUint8, r, c->comm, 0));
+      GG_NCCL(api.GroupEnd());
+    }
+    std::vector<uint8_t> h(2 * hb * c->nranks);
+    GG_CUDA(cudaMemcpy(h.data(), all.p, h.size(), cudaMemcpyDeviceToHost));
+    pc0.assign(1, {});
+    pc1.assign(1, {});
+    for (int r = 0; r < c->nranks; ++r) {
+      if (r == c->rank) continue;
+      void* p0 = nullptr;
+      void* p1 = nullptr;
+      cudaIpcMemHandle_t h0, h1;
+      memcpy(&h0, h.data() + 2 * hb * r, hb);
+      memcpy(&h1, h.data() + 2 * hb * r + hb, hb);
+      GG_CUDA(cudaIpcOpenMemHandle(&p0, h0, cudaIpcMemLazyEnablePeerAccess));
+      GG_CUDA(cudaIpcOpenMemHandle(&p1, h1, cudaIpcMemLazyEnablePeerAccess));
+      opened.push_back(p0);
+      opened.push_back(p1);
+      pc0[0].push_back(p0);
+      pc1[0].push_back(p1);
+    }
+    (void)bytes;
+    return true;
+  }
+  void unmap_peers() override {
+    for (void* q : opened) cudaIpcCloseMemHandle(q);
+    opened.clear();
+  }
   void allreduce2(std::vector<double*>& d, cudaStream_t st) override {
     NcclApi& api = nccl();
     GG_NCCL(api.AllReduce(d[0], d[0], 2, ncclFloat64, ncclSum, c->comm, st));

@@ -496,6 +496,17 @@ static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(co
   pr_edges_seg<CT, true, true, kLoad>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
 }
 
+// Peer contribution buffers of a partitioned run with the fused all-gather:
+// the vertex pass stores every owned next-contribution into each peer's
+// buffer over NVLink (P2P stores into IPC-mapped memory), so no separate
+// all-gather runs (prdist.cuh).  Same global indexing on every rank.
+constexpr int kMaxPeers = 15;
+template <class CT>
+struct PeerSet {
+  CT* p[kMaxPeers];
+  int n;
+};
+
 // vertex pass: rank' = base + d*acc, L1, next dangling mass, next contrib, acc reset.
 // 4 consecutive vertices per thread with 16-byte loads/stores (restrict ->
 // all loads of a group are issued before any store).
@@ -503,21 +514,26 @@ template <class CT>
 __device__ __forceinline__ void pr_vertex_one(int64_t v, const int32_t* __restrict__ outdeg,
                                               double* __restrict__ rank, CT* __restrict__ contrib_next,
                                               double* __restrict__ acc, double base, double damping,
-                                              double& l1, double& dm) {
+                                              double& l1, double& dm, const PeerSet<CT>& peers) {
   const double nv = base + damping * acc[v];
   acc[v] = 0.0;
   l1 += fabs(nv - rank[v]);
   rank[v] = nv;
   const int32_t od = outdeg[v];
-  if (od) contrib_next[v] = (CT)(nv / (double)od);
-  else dm += nv;
+  if (od) {
+    const CT c = (CT)(nv / (double)od);
+    contrib_next[v] = c;
+    for (int k = 0; k < peers.n; ++k) peers.p[k][v] = c;
+  } else {
+    dm += nv;
+  }
 }
 
 template <class CT>
 __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restrict__ outdeg,
                                                double* __restrict__ rank, CT* __restrict__ contrib_next,
                                                double* __restrict__ acc, double* scal, int64_t it,
-                                               double damping, int64_t nglob) {
+                                               double damping, int64_t nglob, const PeerSet<CT>& peers) {
   const double n = (double)nglob;
   const double base = (1.0 - damping) / n + damping * scal[2 * it] / n;
   double l1 = 0, dm = 0;
@@ -548,9 +564,20 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (dg[q]) contrib_next[v + q] = c[q];  // dangling entries are never gathered
+    for (int k = 0; k < peers.n; ++k) {      // fused all-gather: one vector store per peer
+      if (sizeof(CT) == 8) {
+        double2* d = reinterpret_cast<double2*>(peers.p[k] + v);
+        d[0] = make_double2((double)c[0], (double)c[1]);
+        d[1] = make_double2((double)c[2], (double)c[3]);
+      } else {
+        *reinterpret_cast<float4*>(peers.p[k] + v) =
+            make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
+      }
+    }
   }
   for (int64_t v = V4 + tid; v < V; v += nth)
-    pr_vertex_one<CT>(v, outdeg, rank, contrib_next, acc, base, damping, l1, dm);
+    pr_vertex_one<CT>(v, outdeg, rank, contrib_next, acc, base, damping, l1, dm, peers);
+  if (peers.n) __threadfence_system();  // peer stores visible before the exchange's barrier
   l1 = block_sum(l1);
   dm = block_sum(dm);
   if (threadIdx.x == 0) {
@@ -560,10 +587,11 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
 }
 
 template <class CT>
-static __global__ void __launch_bounds__(256) k_pr_vertex(int64_t V, int64_t nglob, const int32_t* outdeg, double* rank,
+static __global__ void __launch_bounds__(256) k_pr_vertex(int64_t V, int64_t nglob, PeerSet<CT> peers,
+                                                          const int32_t* outdeg, double* rank,
                                                           CT* contrib_next, double* acc, double* scal,
                                                           int64_t it, double damping) {
-  pr_vertex_pass<CT>(V, outdeg, rank, contrib_next, acc, scal, it, damping, nglob);
+  pr_vertex_pass<CT>(V, outdeg, rank, contrib_next, acc, scal, it, damping, nglob, peers);
 }
 
 // Whole loop in one cooperative launch (kernel fusion on "s0").
@@ -584,7 +612,9 @@ static __global__ void __launch_bounds__(256) k_prb_fused(const int32_t* src, co
       pr_edges_seg<CT>(src, dst, seg_edge[s], seg_edge[s + 1], cur, acc, 1);
       grid.sync();
     }
-    pr_vertex_pass<CT>(V, outdeg, rank, nxt, acc, scal, it, damping, V);
+    PeerSet<CT> none;
+    none.n = 0;
+    pr_vertex_pass<CT>(V, outdeg, rank, nxt, acc, scal, it, damping, V, none);
     grid.sync();
     l1 = *((volatile double*)scal + 2 * it + 1);
     ++it;
@@ -729,11 +759,16 @@ struct PrRank {
   }
   // owned destinations [lo, hi): rank', L1 partial, next dangling partial,
   // next contrib slice, acc reset
+  // fused all-gather: the peers' contribution buffers (same parity layout)
+  std::vector<CT*> peer_c0, peer_c1;
   void vertex(int64_t it, double damping, cudaStream_t st) {
     const int64_t lo = L->lo, n = L->vloc();
+    PeerSet<CT> ps;
+    ps.n = (int)peer_c0.size();
+    for (int k = 0; k < ps.n; ++k) ps.p[k] = ((it & 1) ? peer_c0[k] : peer_c1[k]) + lo;
     if (n > 0)
-      k_pr_vertex<CT><<<grid_for(n, 256, dev), 256, 0, st>>>(n, V, L->outdeg.p + lo, rank + lo, nxt(it) + lo, acc,
-                                                             scal, it, damping);
+      k_pr_vertex<CT><<<grid_for(n, 256, dev), 256, 0, st>>>(n, V, ps, L->outdeg.p + lo, rank + lo, nxt(it) + lo,
+                                                             acc, scal, it, damping);
     GG_LAUNCH_CHECK();
     ++launches;
   }
@@ -826,6 +861,20 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
   double l1 = INFINITY;
   std::vector<double*> sc(ranks.size());
   std::vector<void*> nx(ranks.size());
+  // fused all-gather through peer memory when the exchange offers it
+  std::vector<void*> c0s, c1s;
+  for (auto* R : ranks) {
+    c0s.push_back(R->c0);
+    c1s.push_back(R->c1);
+  }
+  std::vector<std::vector<void*>> pc0, pc1;
+  const bool p2p = ex.map_peers(c0s, c1s, (size_t)L0->V * sizeof(CT), pc0, pc1);
+  if (p2p)
+    for (size_t i = 0; i < ranks.size(); ++i) {
+      if (pc0[i].size() > (size_t)kMaxPeers) fail(GG_ERR_VALUE, "too many peers for the fused all-gather");
+      for (void* q : pc0[i]) ranks[i]->peer_c0.push_back(static_cast<CT*>(q));
+      for (void* q : pc1[i]) ranks[i]->peer_c1.push_back(static_cast<CT*>(q));
+    }
   while (!(it >= max_iters || l1 < tol)) {
     rt.edge_begin();
     for (auto* R : ranks) R->edges(it, st);
@@ -835,8 +884,8 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
       sc[i] = ranks[i]->scal + 2 * it + 1;
       nx[i] = ranks[i]->nxt(it);
     }
-    ex.allreduce2(sc, st);
-    ex.allgather(nx, sizeof(CT), L0->bounds, st);
+    ex.allreduce2(sc, st);  // also the barrier after which peer stores are visible
+    if (!p2p) ex.allgather(nx, sizeof(CT), L0->bounds, st);
     rt.stats.dispatch_count += 1;
     rt.stats.direction_log.push_back(direction_log);
     ++it;
@@ -844,6 +893,14 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
       GG_CUDA(cudaMemcpyAsync(&l1, ranks[0]->scal + 2 * (it - 1) + 1, 8, cudaMemcpyDeviceToHost, st));
       GG_CUDA(cudaStreamSynchronize(st));
     }
+  }
+  if (p2p) {
+    GG_CUDA(cudaStreamSynchronize(st));
+    for (auto* R : ranks) {
+      R->peer_c0.clear();
+      R->peer_c1.clear();
+    }
+    ex.unmap_peers();
   }
   // every rank's owned rank slice to all ranks
   std::vector<void*> rk(ranks.size());
@@ -856,6 +913,20 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
 // Virtual ranks on one device (test mode for the multi-GPU path): P
 // partitions, each with its own layout and buffers; the exchange copies.
 struct CopyExchange : PrExchange {
+  bool p2p = false;  // the vertex passes store into the other virtual ranks' buffers
+  bool map_peers(const std::vector<void*>& c0s, const std::vector<void*>& c1s, size_t,
+                 std::vector<std::vector<void*>>& pc0, std::vector<std::vector<void*>>& pc1) override {
+    if (!p2p) return false;
+    pc0.assign(c0s.size(), {});
+    pc1.assign(c1s.size(), {});
+    for (size_t i = 0; i < c0s.size(); ++i)
+      for (size_t q = 0; q < c0s.size(); ++q)
+        if (q != i) {
+          pc0[i].push_back(c0s[q]);
+          pc1[i].push_back(c1s[q]);
+        }
+    return true;
+  }
   void allreduce2(std::vector<double*>& d, cudaStream_t st) override {
     std::vector<double> h(2 * d.size());
     for (size_t i = 0; i < d.size(); ++i)
@@ -882,7 +953,7 @@ struct CopyExchange : PrExchange {
 
 template <class CT>
 int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int nparts, int64_t max_iters, double tol,
-                                 double damping, double* ranks_out, Runtime& rt) {
+                                 double damping, double* ranks_out, Runtime& rt, bool fused_allgather) {
   if (nparts < 1) fail(GG_ERR_VALUE, "nparts must be >= 1");
   const int64_t ns = pr_block_window(g, sizeof(CT), s.blocking_size);
   const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
@@ -899,6 +970,7 @@ int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int npart
   }
   if (local_edges != g.E) fail(GG_ERR_ENGINE, "partition lost edges");
   CopyExchange ex;
+  ex.p2p = fused_allgather;
   int64_t it = pagerank_blocked_ranks<CT>(rp, ex, max_iters, tol, damping, s.direction, rt.stream, rt);
   rt.stats.edges_traversed += it * g.E;
   rs[0].unpermute(ranks_out, rt.stream);
@@ -909,9 +981,9 @@ int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int npart
   return it;
 }
 template int64_t pagerank_blocked_virtual<double>(const Graph&, const gg_schedule&, int, int64_t, double, double,
-                                                  double*, Runtime&);
+                                                  double*, Runtime&, bool);
 template int64_t pagerank_blocked_virtual<float>(const Graph&, const gg_schedule&, int, int64_t, double, double,
-                                                 double*, Runtime&);
+                                                 double*, Runtime&, bool);
 
 // One rank of a multi-process run (dist.cu supplies the NCCL exchange).
 template <class CT>

@@ -18,6 +18,16 @@ struct PrExchange {
   virtual void allreduce2(std::vector<double*>& d, cudaStream_t st) = 0;
   virtual void allgather(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
                          cudaStream_t st) = 0;
+  // Fused all-gather: for each rank this process drives (i), the pointers of
+  // every OTHER rank's two contribution buffers (c0s/c1s hold this process's
+  // ranks' own buffers, `bytes` long).  The vertex pass then stores each
+  // owned contribution into all of them (P2P over NVLink) and allgather() is
+  // skipped.  false = not available: allgather() after each vertex pass.
+  virtual bool map_peers(const std::vector<void*>& c0s, const std::vector<void*>& c1s, size_t bytes,
+                         std::vector<std::vector<void*>>& peer_c0, std::vector<std::vector<void*>>& peer_c1) {
+    return false;
+  }
+  virtual void unmap_peers() {}
 };
 
 // Exchange of the partitioned BFS (bfsdist.cu): an element-wise max of an
@@ -39,7 +49,7 @@ int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r
                               int64_t* local_edges);
 template <class CT>
 int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int nparts, int64_t max_iters, double tol,
-                                 double damping, double* ranks_out, Runtime& rt);
+                                 double damping, double* ranks_out, Runtime& rt, bool fused_allgather = false);
 double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r);
 
 }  // namespace gg

@@ -95,15 +95,16 @@ def prepare_dist(nranks, rank, g, program, contrib_fp32=False):
 
 
 def pagerank_virtual(g, nparts, program, max_iters=100, tolerance=1e-9, damping=0.85,
-                     out=None, contrib_fp32=False):
+                     out=None, contrib_fp32=False, fused_allgather=False):
     """The partitioned EdgeBlocking run with `nparts` virtual ranks on one
-    device (copy exchange) -- the test mode of the multi-GPU path."""
+    device -- the test mode of the multi-GPU path: copy exchange, or the
+    vertex pass storing into the other ranks' buffers (fused all-gather)."""
     ranks = out if out is not None else np.empty(g.num_vertices, np.float64)
     st = _lib.new_stats()
     pod = _binding(program)
     _lib.call("gg_pagerank_virtual", g.handle, int(nparts), C.byref(pod),
-              1 if contrib_fp32 else 0, int(max_iters), float(tolerance), float(damping),
-              _lib.ptr(ranks), C.byref(st))
+              1 if contrib_fp32 else 0, 1 if fused_allgather else 0, int(max_iters),
+              float(tolerance), float(damping), _lib.ptr(ranks), C.byref(st))
     return ranks, RunStats.from_pod(st)
 
 

@@ -29,9 +29,10 @@ def _eb_program(gg, blocking_size=None):
                                                     blocking_size=blocking_size)})
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("fp32", [False, True])
 @pytest.mark.parametrize("nparts", [1, 2, 3, 4, 8])
-def test_pagerank_virtual_ranks_match_oracle(nparts, fp32):
+def test_pagerank_virtual_ranks_match_oracle(nparts, fp32, fused):
     """The partitioned EdgeBlocking run (per-rank layouts over owned
     destinations + exchange) with virtual ranks on one device."""
     import paper_2012_07990_b200 as gg
@@ -41,7 +42,7 @@ def test_pagerank_virtual_ranks_match_oracle(nparts, fp32):
     want, _ = oracle.pagerank(V, s, d, 20, 0.0)
     for bs in (None, 300):  # default window (hot segment only) and many cold segments
         ranks, st = pagerank_virtual(g, nparts, _eb_program(gg, bs), max_iters=20, tolerance=0.0,
-                                     contrib_fp32=fp32)
+                                     contrib_fp32=fp32, fused_allgather=fused)
         assert np.max(np.abs(ranks - want) / want) < 1e-6, (nparts, bs)
         assert st.rounds == 20
         assert st.edges_traversed == 20 * len(s)
@@ -55,7 +56,8 @@ def test_pagerank_virtual_ranks_tolerance_and_tiny_partitions():
     V, s, d = gen.rmat(6, 4, seed=9)
     g = gg.Graph.from_coo(V, s, d)
     want, it = oracle.pagerank(V, s, d, 100, 1e-9)
-    ranks, st = pagerank_virtual(g, 8, _eb_program(gg), max_iters=100, tolerance=1e-9)
+    ranks, st = pagerank_virtual(g, 8, _eb_program(gg), max_iters=100, tolerance=1e-9,
+                                 fused_allgather=True)
     assert np.max(np.abs(ranks - want) / want) < 1e-6
     assert st.rounds == it
 
