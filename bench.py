@@ -370,7 +370,9 @@ def main():
                        "includes": "H2D of COO from pinned host memory, device graph build "
                                    "(EdgeBlocking prep), 20 iterations, D2H of ranks"}
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_pagerank_sample(min(args.cpu_scale, scale), ef, seed)
+        # bounded sample: ~10 s of PageRank iterations on the host cores
+        line["cpu_baseline"] = cpu_pagerank_sample(min(args.cpu_scale, scale), ef, seed,
+                                                   budget_s=10.0, max_iters=10000)
     if rank == 0:
         print(json.dumps(line))
     if comm is not None:
