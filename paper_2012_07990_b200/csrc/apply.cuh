@@ -93,7 +93,7 @@ void run_pull(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
     case GG_LB_STRICT: {
       const int64_t nspans = std::min<int64_t>(V > 0 ? V : 1, (int64_t)sm_count(dev) * 2048);
       strict_spans(rt, nspans);
-      k_pull_strict<Op><<<grid_for(nspans, 256, dev), 256, 0, st>>>(a, rt->spans.p, nspans);
+      k_pull_strict<Op><<<grid_for(nspans * 32, 256, dev), 256, 0, st>>>(a, rt->spans.p, nspans);
       break;
     }
     case GG_LB_TWC: {

@@ -657,25 +657,25 @@ __device__ __forceinline__ typename Op::Acc block_reduce(typename Op::Acc acc) {
   return r;
 }
 
-// CM: CTAs take contiguous destination chunks; each destination's in-list is
-// reduced by the whole CTA.
+// CM: CTAs take contiguous destination chunks (engine.py:160-164, even
+// split, earlier chunks take the extra); inside its chunk a CTA's threads own
+// destinations cyclically, each reducing its in-list with early exit.
 template <class Op>
 __device__ __forceinline__ void b_pull_cm(PullArgs<Op> a) {
-  __shared__ int s_keep;
-  const int64_t chunk = (a.g.V + gridDim.x - 1) / gridDim.x;
+  const int64_t V = a.g.V;
+  const int64_t base = V / gridDim.x, extra = V % gridDim.x;
+  const int64_t b = blockIdx.x;
+  const int64_t start = b * base + min(b, extra);
+  const int64_t end = start + base + (b < extra ? 1 : 0);
   int64_t sc = 0;
-  for (int64_t v = blockIdx.x * chunk; v < min(a.g.V, (blockIdx.x + 1) * chunk); ++v) {
-    if (threadIdx.x == 0) s_keep = !a.use_filter || a.op.filter((int32_t)v);
-    __syncthreads();
-    bool keep = s_keep;
-    __syncthreads();
-    if (!keep) continue;
+  for (int64_t v = start + threadIdx.x; v < end; v += blockDim.x) {
+    if (a.use_filter && !a.op.filter((int32_t)v)) continue;
     int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
-    if (threadIdx.x == 0) sc += hi - lo;
+    sc += hi - lo;
     typename Op::Acc acc = a.op.init();
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) pull_visit(a, acc, (int32_t)v, e);
-    acc = block_reduce<Op>(acc);
-    if (threadIdx.x == 0) a.op.finish((int32_t)v, acc, a.out);
+    for (int64_t e = lo; e < hi; ++e)
+      if (pull_visit(a, acc, (int32_t)v, e)) break;
+    a.op.finish((int32_t)v, acc, a.out);
   }
   add_scanned(a.scanned, sc);
 }
@@ -690,10 +690,12 @@ __global__ void __launch_bounds__(256) k_pull_cm(PullArgs<Op> a) {
 template <class Op>
 __device__ __forceinline__ void b_pull_strict(PullArgs<Op> a, const int64_t* span_start,
                                                      int64_t nspans) {
+  // one warp per span; its lanes own the span's destinations cyclically
   int64_t sc = 0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nspans;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    for (int64_t v = span_start[t]; v < span_start[t + 1]; ++v) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < nspans; t += nw) {
+    for (int64_t v = span_start[t] + lane_id(); v < span_start[t + 1]; v += kWarp) {
       if (a.use_filter && !a.op.filter((int32_t)v)) continue;
       int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
       sc += hi - lo;
