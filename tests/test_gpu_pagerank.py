@@ -150,3 +150,36 @@ def test_pagerank_edge_blocking_hub_source_beyond_smem_cache(gg):
         sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True)
         r = gg.pagerank(g, program_with(sch), max_iters=15, tolerance=0.0, contrib_fp32=fp32)
         assert max_rel_err(r.array, want) < PR_TOL
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+@pytest.mark.parametrize("case", ["single", "no_edges", "self_loops", "one_source", "ragged"])
+def test_pagerank_edge_blocking_edge_cases(gg, case, fp32):
+    """Empty and ragged inputs under EdgeBlocking (single vertex, edgeless,
+    self-loops only, one source, V not a multiple of the vector width) vs
+    the oracle, also with virtual ranks."""
+    from paper_2012_07990_b200.dist import pagerank_virtual
+    rng = np.random.default_rng(7)
+    if case == "single":
+        V, s, d = 1, np.array([0]), np.array([0])
+    elif case == "no_edges":
+        V, s, d = 7, np.zeros(0, np.int64), np.zeros(0, np.int64)
+    elif case == "self_loops":
+        V = 9
+        s = d = np.arange(V)
+    elif case == "one_source":
+        V = 1000
+        s, d = np.zeros(500, np.int64), rng.integers(0, V, 500)
+    else:
+        V = 4099
+        s, d = rng.integers(0, V, 20000), rng.integers(0, V, 20000)
+    g = gg.Graph.from_coo(V, s, d)
+    want, _ = oracle.pagerank(V, s, d, 15, 0.0)
+    for bs in (None, 3):
+        sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True, blocking_size=bs)
+        r = gg.pagerank(g, program_with(sch), max_iters=15, tolerance=0.0, contrib_fp32=fp32)
+        assert max_rel_err(r.array, want) < PR_TOL, (case, bs)
+        if V >= 2:
+            ranks, _ = pagerank_virtual(g, 3, program_with(sch), max_iters=15, tolerance=0.0,
+                                        contrib_fp32=fp32, fused_allgather=True)
+            assert max_rel_err(ranks, want) < PR_TOL, (case, bs, "virtual")
