@@ -13,6 +13,7 @@
 // Fused (s0 kernel fusion): the whole loop, including advance(), is ONE
 // cooperative launch with per-bucket frontiers and grid barriers.
 #include "fused.cuh"
+#include <cstdio>
 
 namespace gg {
 
@@ -82,7 +83,15 @@ struct SsspFusedArgs {
   unsigned long long* scanned;
   long long* counters;            // [0] rounds [1] relax rounds
   int cta;
+  unsigned long long* prof;       // GG_SSSP_PROFILE: [0] top-barrier wait [1] prep+barrier
+                                  // [2] max edge-phase time of any thread per round (summed) (ns)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -95,8 +104,14 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
   // after the top barrier, so a queue's count can be reset by thread 0 as
   // soon as nobody reads it any more; the advance's minimum alternates
   // between two slots, the unused one re-armed for the next advance.
+  unsigned long long t0 = a.prof ? gtime() : 0;
   while (true) {
     grid.sync();
+    unsigned long long t1 = 0;
+    if (a.prof && tid == 0) {
+      t1 = gtime();
+      a.prof[0] += t1 - t0;
+    }
     const unsigned long long ncur = *((volatile unsigned long long*)a.qn + cur);
     const unsigned long long nfar = *((volatile unsigned long long*)a.qn + far);
     if (ncur == 0 && nfar == 0) break;  // BucketQueue.done()
@@ -135,6 +150,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
       }
       ++advances;
       int t = far; far = far2; far2 = t;
+      if (a.prof) t0 = gtime();
       continue;
     }
     // take_current(): the pending bucket becomes the relax input; the new
@@ -154,6 +170,8 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
       iv.count = a.qn + take;
     }
     grid.sync();
+    unsigned long long t2 = a.prof ? gtime() : 0;
+    if (a.prof && tid == 0) a.prof[1] += t2 - t1;
     OpRelax op{a.dist, a.delta, index, OutBuilder{}, OutBuilder{}};
     op.cur.mode = op.far.mode = GG_CREATE_FUSED;
     op.cur.dedup = op.far.dedup = DEDUP_MARK_BYTES;
@@ -162,6 +180,11 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
     OutBuilder none{};
     none.mode = OUT_NONE;
     fused_edge_phase(a.s, a.out, a.out, a.coo, iv, op, none, false, a.scanned, a.sc, a.cta, grid);
+    if (a.prof) {
+      const unsigned long long t3 = gtime();
+      if (relax < 1024) atomicMax(a.prof + 3 + relax, t3 - t2);  // slowest thread of the round
+      t0 = t3;
+    }
     if (a.s.load_balance == GG_LB_EDGE_ONLY) {
       grid.sync();  // membership is read by the edge phase
       for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 0;
@@ -237,6 +260,12 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
     a.scanned = rt.scanned.p;
     a.counters = counters.p;
     a.cta = rt.cfg.cta_size;
+    DevBuf<unsigned long long> prof;
+    if (getenv("GG_SSSP_PROFILE")) {
+      prof.alloc(3 + 1024);
+      prof.zero(st);
+      a.prof = prof.p;
+    }
     int blocks = max_coop_blocks((const void*)k_sssp_fused, 256, dev);
     FusedHost fh;
     const gg_schedule* ss[1] = {&s};
@@ -250,6 +279,16 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
     long long h[2];
     GG_CUDA(cudaMemcpyAsync(h, counters.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     GG_CUDA(cudaStreamSynchronize(st));
+    if (a.prof) {  // diagnostic: where a fused round's time goes (stderr)
+      std::vector<unsigned long long> hp(3 + 1024);
+      GG_CUDA(cudaMemcpy(hp.data(), prof.p, hp.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long mx = 0;
+      for (int k = 0; k < 1024; ++k) mx += hp[3 + k];
+      const long long nr = h[1] < 1024 ? h[1] : 1024;
+      fprintf(stderr, "sssp fused profile: rounds %lld relax %lld | thread0: top-barrier wait %.3f ms, "
+              "prep+barrier %.3f ms | slowest-thread edge phase, mean of first %lld rounds: %.3f us\n",
+              h[0], h[1], hp[0] / 1e6, hp[1] / 1e6, nr, nr ? mx / 1e3 / nr : 0.0);
+    }
     rt.stats.dispatch_count += 1;
     rt.stats.rounds += h[0];
     for (long long k = 0; k < h[1]; ++k) rt.stats.direction_log.push_back(GG_PUSH);
