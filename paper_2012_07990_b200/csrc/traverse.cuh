@@ -209,12 +209,19 @@ __device__ __forceinline__ void b_push_wm(PushArgs<Op> a) {
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // even contiguous split of the active list over warps, earlier warps take
+  // the extra (engine.py:167-176, partition_even_chunks :32-44): a small
+  // frontier spreads its edges over many warps (one edge per lane) instead
+  // of queueing them behind one another
+  const int64_t per = n / nwarps, extra = n % nwarps;
+  const int64_t wstart = warp * per + min(warp, extra);
+  const int64_t wend = wstart + per + (warp < extra ? 1 : 0);
   int64_t sc = 0;
-  for (int64_t base = warp * kWarp; base < n; base += nwarps * kWarp) {
+  for (int64_t base = wstart; base < wend; base += kWarp) {
     int64_t i = base + lane;
     int32_t u = -1;
     int64_t lo = 0, deg = 0;
-    if (i < n) {
+    if (i < wend) {
       u = active_at(a.in, i);
       lo = __ldg(a.g.off + u);
       deg = __ldg(a.g.off + u + 1) - lo;
