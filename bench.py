@@ -70,7 +70,7 @@ def parse():
     p.add_argument("--fusion", action="store_true", help="c2: fused loop")
     p.add_argument("--side", type=int, default=None, help="c3 grid side")
     p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")
-    p.add_argument("--lb", default="ETWC", help="c3 load balance")
+    p.add_argument("--lb", default="WM", help="c3 load balance (swept: WM best)")
     p.add_argument("--no-fusion", action="store_true", help="c3: unfused loop")
     p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED,EB",
                    help="c4 load balances (EB = EDGE_ONLY+BLOCKED, EDGE = EDGE_ONLY)")

@@ -5,7 +5,7 @@
 
 namespace gg {
 
-int max_coop_blocks(const void* fn, int block, int dev, size_t smem = 0);
+int max_coop_blocks(const void* fn, int block, int dev, size_t smem = 0, int cap_per_sm = 0);
 void strict_prefix(Runtime* rt, const InView& in, int64_t n);
 void strict_spans(Runtime* rt, int64_t nspans);
 void clear_marks(Runtime* rt, Frontier* out, const OutBuilder& ob);

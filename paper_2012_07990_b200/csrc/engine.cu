@@ -450,12 +450,14 @@ void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n) {
   *n = rt->etwc_n.p;
 }
 
-int max_coop_blocks(const void* fn, int block, int dev, size_t smem) {
+int max_coop_blocks(const void* fn, int block, int dev, size_t smem, int cap_per_sm) {
   int per_sm = 0;
   GG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
   if (per_sm < 1) fail(GG_ERR_CUDA, "kernel cannot be co-resident");
-  // grid-barrier cost grows with the CTA count; GG_COOP_PER_SM caps the
-  // resident CTAs per SM of cooperative (fused-loop) launches
+  // a grid barrier costs ~1.2 us at 1-2 CTAs/SM and ~2.5 us at 8 (measured,
+  // profiles/r01/microbench_gridsync.txt): latency-bound fused loops cap the
+  // resident CTAs per SM; GG_COOP_PER_SM overrides every cooperative launch
+  if (cap_per_sm >= 1 && cap_per_sm < per_sm) per_sm = cap_per_sm;
   if (const char* e = getenv("GG_COOP_PER_SM")) {
     int cap = atoi(e);
     if (cap >= 1 && cap < per_sm) per_sm = cap;

@@ -311,7 +311,7 @@ void bfs_fused(Runtime& rt, const gg_binding& b, int32_t* parent, int32_t source
   a.log_cap = log_cap;
   a.counters = counters.p;
   a.cta = rt.cfg.cta_size;
-  int blocks = max_coop_blocks((const void*)k_bfs_fused, 256, rt.dev);
+  int blocks = max_coop_blocks((const void*)k_bfs_fused, 256, rt.dev, 0, 2);
   FusedHost fh;
   fh.prepare(rt, ss, ns, blocks);
   a.sc = fh.sc;

@@ -78,6 +78,7 @@ struct SsspFusedArgs {
   unsigned long long* qn;         // counts [4]
   uint8_t* cmark;
   uint8_t* fmark;
+  int32_t* stamps;                // fused relax rounds: current-bucket dedup by round stamp
   uint8_t* member;                // EDGE_ONLY input membership (boolmap)
   unsigned long long* best;       // advance scratch
   unsigned long long* scanned;
@@ -132,8 +133,9 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
       if (best != kUnreached) {
         OutBuilder oc{}, of{};
         oc.mode = of.mode = GG_CREATE_FUSED;
-        oc.dedup = of.dedup = DEDUP_MARK_BYTES;
-        oc.queue = a.q[cur]; oc.qcount = a.qn + cur; oc.mark_bytes = a.cmark;
+        oc.dedup = DEDUP_NONE;  // far holds each vertex once (fmark), so the split does too
+        of.dedup = DEDUP_MARK_BYTES;
+        oc.queue = a.q[cur]; oc.qcount = a.qn + cur;
         of.queue = a.q[far2]; of.qcount = a.qn + far2; of.mark_bytes = a.fmark;
         for (int64_t i = tid; i < (int64_t)nfar; i += nth) {
           int32_t v = a.q[far][i];
@@ -153,29 +155,35 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
       if (a.prof) t0 = gtime();
       continue;
     }
-    // take_current(): the pending bucket becomes the relax input; the new
-    // current queue (the previous input) is no longer read by anyone
+    // take_current(): the pending bucket becomes the relax input.  One grid
+    // barrier per relax round: the input's size is the register ncur (its
+    // counter is not read again, so thread 0 zeroes it now -- it is the next
+    // round's output), and the output's per-round dedup is a round stamp
+    // (no marks to clear).  EDGE_ONLY needs its membership boolmap set first.
     { int t = cur; cur = take; take = t; }
-    if (tid == 0) a.qn[cur] = 0;
-    for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.cmark[a.q[take][i]] = 0;
+    if (tid == 0) a.qn[take] = 0;
     InView iv{};
     iv.coherent = 1;
     if (a.s.load_balance == GG_LB_EDGE_ONLY) {
       for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 1;
       iv.repr = GG_BOOLMAP;
       iv.bools = a.member;
+      grid.sync();
     } else {
       iv.repr = GG_SPARSE;
       iv.ids = a.q[take];
       iv.count = a.qn + take;
+      iv.n_fixed = (int64_t)ncur;
     }
-    grid.sync();
     unsigned long long t2 = a.prof ? gtime() : 0;
     if (a.prof && tid == 0) a.prof[1] += t2 - t1;
     OpRelax op{a.dist, a.delta, index, OutBuilder{}, OutBuilder{}};
     op.cur.mode = op.far.mode = GG_CREATE_FUSED;
-    op.cur.dedup = op.far.dedup = DEDUP_MARK_BYTES;
-    op.cur.queue = a.q[cur]; op.cur.qcount = a.qn + cur; op.cur.mark_bytes = a.cmark;
+    op.cur.dedup = DEDUP_COUNTERS;
+    op.cur.stamps = a.stamps;
+    op.cur.round = (int32_t)(relax + 1);
+    op.far.dedup = DEDUP_MARK_BYTES;
+    op.cur.queue = a.q[cur]; op.cur.qcount = a.qn + cur;
     op.far.queue = a.q[far]; op.far.qcount = a.qn + far; op.far.mark_bytes = a.fmark;
     OutBuilder none{};
     none.mode = OUT_NONE;
@@ -251,6 +259,9 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
     GG_CUDA(cudaMemcpyAsync(qn.p, &n1, 8, cudaMemcpyHostToDevice, st));
     DevBuf<uint8_t> member(mb);
     member.zero(st);
+    DevBuf<int32_t> stamps(V);
+    stamps.zero(st);
+    a.stamps = stamps.p;
     DevBuf<long long> counters(2);
     a.qn = qn.p;
     a.cmark = cmark.p;
@@ -266,7 +277,7 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
       prof.zero(st);
       a.prof = prof.p;
     }
-    int blocks = max_coop_blocks((const void*)k_sssp_fused, 256, dev);
+    int blocks = max_coop_blocks((const void*)k_sssp_fused, 256, dev, 0, 1);  // barrier-bound
     FusedHost fh;
     const gg_schedule* ss[1] = {&s};
     fh.prepare(rt, ss, 1, blocks);

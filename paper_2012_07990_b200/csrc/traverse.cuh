@@ -47,8 +47,9 @@ struct InView {
   const uint32_t* bits;
   const uint8_t* bools;
   int coherent = 0;  // fused loops: membership written earlier in the same launch
+  int64_t n_fixed = -1;  // SPARSE size known to every thread (fused loops): *count unread
 
-  __device__ __forceinline__ int64_t size() const { return (int64_t)*count; }
+  __device__ __forceinline__ int64_t size() const { return n_fixed >= 0 ? n_fixed : (int64_t)*count; }
   __device__ __forceinline__ bool member(int32_t u) const {
     if (repr == GG_BITMAP)
       return ((coherent ? __ldcg(bits + (u >> 5)) : __ldg(bits + (u >> 5))) >> (u & 31)) & 1u;
