@@ -74,8 +74,8 @@ struct SsspFusedArgs {
   FusedScratch sc;
   unsigned long long* dist;
   unsigned long long delta;
-  int32_t* q[4];                  // current, take, far, far2
-  unsigned long long* qn;         // counts [4]
+  int32_t* q[5];                  // current-bucket ring [0..2], far pair [3..4]
+  unsigned long long* qn;         // counts [5]
   uint8_t* cmark;
   uint8_t* fmark;
   int32_t* stamps;                // fused relax rounds: current-bucket dedup by round stamp
@@ -98,13 +98,17 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  int cur = 0, take = 1, far = 2, far2 = 3;
+  // Queues: a ring of three for the current bucket (q[0..2]) and a pair for
+  // far (q[3], q[4]).  One grid barrier per relax round: every thread reads
+  // the counts right after the barrier; a relax round reads ring slot `ci`
+  // (its size stays in a register), appends to slot ci+1, and thread 0
+  // zeroes slot ci+2 -- the previous round's input, which nobody reads or
+  // writes in this round and which becomes the next round's output.  The
+  // output's per-round dedup is a round stamp (no marks to clear).  An
+  // advance refills the (empty) current slot behind its own barrier.
+  int ci = 0, far = 3, far2 = 4;
   unsigned long long index = 0;
   long long rounds = 0, relax = 0, advances = 0;
-  // Two grid barriers per round.  Counts are captured in registers right
-  // after the top barrier, so a queue's count can be reset by thread 0 as
-  // soon as nobody reads it any more; the advance's minimum alternates
-  // between two slots, the unused one re-armed for the next advance.
   unsigned long long t0 = a.prof ? gtime() : 0;
   while (true) {
     grid.sync();
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
       t1 = gtime();
       a.prof[0] += t1 - t0;
     }
-    const unsigned long long ncur = *((volatile unsigned long long*)a.qn + cur);
+    const unsigned long long ncur = *((volatile unsigned long long*)a.qn + ci);
     const unsigned long long nfar = *((volatile unsigned long long*)a.qn + far);
     if (ncur == 0 && nfar == 0) break;  // BucketQueue.done()
     ++rounds;
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
         oc.mode = of.mode = GG_CREATE_FUSED;
         oc.dedup = DEDUP_NONE;  // far holds each vertex once (fmark), so the split does too
         of.dedup = DEDUP_MARK_BYTES;
-        oc.queue = a.q[cur]; oc.qcount = a.qn + cur;
+        oc.queue = a.q[ci]; oc.qcount = a.qn + ci;
         of.queue = a.q[far2]; of.qcount = a.qn + far2; of.mark_bytes = a.fmark;
         for (int64_t i = tid; i < (int64_t)nfar; i += nth) {
           int32_t v = a.q[far][i];
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
         index = best;
       }
       if (tid == 0) {
-        a.qn[far] = 0;                         // count read into registers above
+        a.qn[far] = 0;                            // read into registers before the barrier
         a.best[(advances + 1) & 1] = kUnreached;  // next advance's slot
       }
       ++advances;
@@ -155,24 +159,19 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
       if (a.prof) t0 = gtime();
       continue;
     }
-    // take_current(): the pending bucket becomes the relax input.  One grid
-    // barrier per relax round: the input's size is the register ncur (its
-    // counter is not read again, so thread 0 zeroes it now -- it is the next
-    // round's output), and the output's per-round dedup is a round stamp
-    // (no marks to clear).  EDGE_ONLY needs its membership boolmap set first.
-    { int t = cur; cur = take; take = t; }
-    if (tid == 0) a.qn[take] = 0;
+    const int in = ci, out = ci == 2 ? 0 : ci + 1, spare = ci == 0 ? 2 : ci - 1;
+    if (tid == 0) a.qn[spare] = 0;
     InView iv{};
     iv.coherent = 1;
     if (a.s.load_balance == GG_LB_EDGE_ONLY) {
-      for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 1;
+      for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[in][i]] = 1;
       iv.repr = GG_BOOLMAP;
       iv.bools = a.member;
       grid.sync();
     } else {
       iv.repr = GG_SPARSE;
-      iv.ids = a.q[take];
-      iv.count = a.qn + take;
+      iv.ids = a.q[in];
+      iv.count = a.qn + in;
       iv.n_fixed = (int64_t)ncur;
     }
     unsigned long long t2 = a.prof ? gtime() : 0;
@@ -183,7 +182,7 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
     op.cur.stamps = a.stamps;
     op.cur.round = (int32_t)(relax + 1);
     op.far.dedup = DEDUP_MARK_BYTES;
-    op.cur.queue = a.q[cur]; op.cur.qcount = a.qn + cur;
+    op.cur.queue = a.q[out]; op.cur.qcount = a.qn + out;
     op.far.queue = a.q[far]; op.far.qcount = a.qn + far; op.far.mark_bytes = a.fmark;
     OutBuilder none{};
     none.mode = OUT_NONE;
@@ -195,8 +194,9 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
     }
     if (a.s.load_balance == GG_LB_EDGE_ONLY) {
       grid.sync();  // membership is read by the edge phase
-      for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[take][i]] = 0;
+      for (int64_t i = tid; i < (int64_t)ncur; i += nth) a.member[a.q[in][i]] = 0;
     }
+    ci = out;
     ++relax;
   }
   if (tid == 0) {
@@ -246,11 +246,11 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
     a.out.V = V;
     a.dist = dist.p;
     a.delta = delta;
-    DevBuf<int32_t> q[4];
-    DevBuf<unsigned long long> qn(4), best(2);
+    DevBuf<int32_t> q[5];
+    DevBuf<unsigned long long> qn(5), best(2);
     qn.zero(st);
     GG_CUDA(cudaMemsetAsync(best.p, 0xff, 2 * sizeof(unsigned long long), st));
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
       q[k].alloc(V + 1);
       a.q[k] = q[k].p;
     }
