@@ -167,7 +167,19 @@ def cc_bc_c4(gg, args, peak):
     bc_sources = _pick_sources(deg, args.sources or 4, 6)
     cc_res, bc_res = {}, {}
     for lb in lbs:
-        # "EB" = EDGE_ONLY + BLOCKED (EdgeBlocking, blocking.py:78-186), "EDGE" = EDGE_ONLY
+        # "EB" = EDGE_ONLY + BLOCKED (EdgeBlocking, blocking.py:78-186), "EDGE" = EDGE_ONLY,
+        # "HYBRID" = BC only: PUSH+ETWC below 1% of V, PULL+BITMAP above (CC takes no hybrid)
+        if lb == "HYBRID":
+            hy = gg.HybridSchedule(threshold=0.01,
+                                   s1=gg.Schedule(direction="PUSH", load_balance="ETWC"),
+                                   s2=gg.Schedule(direction="PULL", pull_frontier_repr="BITMAP",
+                                                  frontier_creation="UNFUSED_BITMAP"))
+            progh = gg.ScheduleProgram({"s0:s1": hy})
+            gg.bc(g, bc_sources[:1], progh, out=scores)
+            r = gg.bc(g, bc_sources, progh, out=scores)
+            bc_res[lb] = {"ms": r.stats.kernel_ms, "rounds": r.stats.rounds,
+                          "edges_traversed": r.stats.edges_traversed}
+            continue
         if lb == "EB":
             sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True)
         elif lb == "EDGE":
