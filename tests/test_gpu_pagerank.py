@@ -183,3 +183,22 @@ def test_pagerank_edge_blocking_edge_cases(gg, case, fp32):
             ranks, _ = pagerank_virtual(g, 3, program_with(sch), max_iters=15, tolerance=0.0,
                                         contrib_fp32=fp32, fused_allgather=True)
             assert max_rel_err(ranks, want) < PR_TOL, (case, bs, "virtual")
+
+
+def test_integration_md_reference_side_stub():
+    """The ctypes stub INTEGRATION.md tells a schedge maintainer to add runs
+    as written (library path substituted) and matches the oracle."""
+    import re
+    import types
+    from tests.conftest import ROOT
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"## 2\. Binding.*?```python\n(.*?)```", text, re.S).group(1)
+    code = code.replace("/path/to/paper_2012_07990_b200/libgg.so",
+                        os.path.join(ROOT, "paper_2012_07990_b200", "libgg.so"))
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    V, s, d = gen.rmat(10, 8, seed=13)
+    g = types.SimpleNamespace(num_vertices=V, coo_src=s.tolist(), coo_dst=d.tolist(), symmetric=False)
+    got = ns["pagerank"](g, 20, 0.0, 0.85)
+    want, _ = oracle.pagerank(V, s, d, 20, 0.0)
+    assert max_rel_err(got, want) < PR_TOL
