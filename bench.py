@@ -67,7 +67,7 @@ def parse():
                    help="c2: s1 with MONOTONIC_COUNTERS dedup (default off: the BFS CAS "
                         "already admits each vertex once, so the frontier is identical)")
     p.add_argument("--pull-lb", default="VERTEX_BASED", help="c2 pull-side load balance")
-    p.add_argument("--fusion", action="store_true", help="c2: fused loop")
+    p.add_argument("--fusion", action="store_true", help="c1/c2/c5: fused loop (s0 kernel fusion)")
     p.add_argument("--side", type=int, default=None, help="c3 grid side")
     p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")
     p.add_argument("--lb", default="WM", help="c3 load balance (swept: WM best)")
@@ -223,6 +223,8 @@ def main():
     V, E = g.num_vertices, g.num_edges
     sch = gg.Schedule(**SCHEDULES[args.schedule])
     prog = gg.ScheduleProgram({"s0:s1": sch})
+    if args.fusion:  # s0 loop fusion: the whole 20-iteration loop is one cooperative launch
+        prog.bindings["s0"] = gg.Schedule(kernel_fusion=True)
     import ctypes as C
     from paper_2012_07990_b200 import _lib
     from paper_2012_07990_b200.engine import binding_pod
