@@ -319,7 +319,8 @@ def main():
             "data": "synthetic RMAT generated on device (sort_by_source%s)"
                     % (", permuted ids" if args.permute else ", natural ids"),
             "config": {"workload": workload, "V": V, "E": E, "iterations": iters,
-                       "schedule": SCHEDULES[args.schedule], "blocking_prep_ms": prep_ms,
+                       "schedule": dict(SCHEDULES[args.schedule], kernel_fusion=bool(args.fusion)),
+                       "blocking_prep_ms": prep_ms,
                        "parallelism": ("1-D destination partition x%d, NCCL allgather of "
                                        "contributions per iteration" % world) if world > 1
                                       else "single GPU",
