@@ -138,6 +138,14 @@ inline unsigned grid_for(int64_t work, int block, int dev, int per_sm = 8) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
 
+// Load of data written earlier in the same cooperative launch, separated by
+// a grid barrier: cg::grid_group::sync fences (CCTL.IVALL: the SM's L1 is
+// invalidated after its last block arrives), so a plain L1-cached load sees
+// the pre-barrier writes -- unlike ld.global.nc, which may serve stale data
+// for the launch's lifetime, and unlike ld.global.cg, which skips L1.
+template <class T>
+__device__ __forceinline__ T ld_fresh(const T* p) { return *p; }
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -395,7 +395,7 @@ __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const in
              : su[q] < nhot ? (double)s_hot[su[q]]
              : (double)ld_gather<kLoad>(contrib + su[q]);
     else
-      v[q] = dv[q] < 0 ? 0.0 : (double)(coherent ? __ldcg(contrib + su[q]) : __ldg(contrib + su[q]));
+      v[q] = dv[q] < 0 ? 0.0 : (double)(coherent ? ld_fresh(contrib + su[q]) : __ldg(contrib + su[q]));
   }
   // in-lane runs: head run (may continue the previous lane), complete middle
   // runs (emitted here), tail run (joined across lanes by the scan)

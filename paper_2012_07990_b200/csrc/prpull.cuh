@@ -214,7 +214,7 @@ __device__ __forceinline__ void pr_pull_chunks(const PrPullArgs<CT>& a, int64_t 
       }
 #pragma unroll
       for (int q = 0; q < kU; ++q)
-        val[q] = uv[q] >= 0 ? (double)(a.coherent ? __ldcg(a.contrib + uv[q]) : __ldg(a.contrib + uv[q]))
+        val[q] = uv[q] >= 0 ? (double)(a.coherent ? ld_fresh(a.contrib + uv[q]) : __ldg(a.contrib + uv[q]))
                             : 0.0;
 #pragma unroll
       for (int q = 0; q < kU; ++q) {

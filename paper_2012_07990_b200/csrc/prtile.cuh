@@ -72,7 +72,7 @@ __device__ __forceinline__ void pr_tiles(const TileArgs<CT>& a, int64_t it, doub
     for (int q = 0; q < kIpt; ++q) {
       const int j = tid + q * kTileThreads;
       if (us[q] >= 0)
-        s_val[j] = (double)(a.coherent ? __ldcg(a.contrib + us[q]) : __ldg(a.contrib + us[q]));
+        s_val[j] = (double)(a.coherent ? ld_fresh(a.contrib + us[q]) : __ldg(a.contrib + us[q]));
     }
     __syncthreads();
     // 3. merge walk: start coordinate by binary search on the diagonal

@@ -52,8 +52,8 @@ struct InView {
   __device__ __forceinline__ int64_t size() const { return n_fixed >= 0 ? n_fixed : (int64_t)*count; }
   __device__ __forceinline__ bool member(int32_t u) const {
     if (repr == GG_BITMAP)
-      return ((coherent ? __ldcg(bits + (u >> 5)) : __ldg(bits + (u >> 5))) >> (u & 31)) & 1u;
-    if (repr == GG_BOOLMAP) return (coherent ? __ldcg(bools + u) : __ldg(bools + u)) != 0;
+      return ((coherent ? ld_fresh(bits + (u >> 5)) : __ldg(bits + (u >> 5))) >> (u & 31)) & 1u;
+    if (repr == GG_BOOLMAP) return (coherent ? ld_fresh(bools + u) : __ldg(bools + u)) != 0;
     return true;  // all active
   }
 };
