@@ -143,6 +143,7 @@ template <class Op>
 std::unique_ptr<Frontier> apply_op(Runtime* rt, const Op& op, bool use_filter,
                                           std::unique_ptr<Frontier>* input, const gg_binding& b,
                                           bool reuse, bool collect_output) {
+  NvtxRange nvtx("gg.edgeset_apply");
   check_binding(b);
   const Graph* g = rt->g;
   Frontier* in = input ? input->get() : nullptr;

@@ -1,6 +1,7 @@
 // common.cuh — error plumbing, device buffers and warp/block primitives shared
 // by every translation unit of libgg.so (sm_100a only).
 #pragma once
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys/ncu timelines
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -116,6 +117,13 @@ struct DeviceGuard {
     if (prev != dev) GG_CUDA(cudaSetDevice(dev));
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// RAII NVTX range (SURVEY §5 tracing): the driver phases show up named in
+// nsys / ncu --nvtx timelines; a no-op without a profiler attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 inline double now_ms() {

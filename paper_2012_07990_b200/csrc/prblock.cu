@@ -199,6 +199,7 @@ static void sort_edges(const Graph& g, PrBlockLayout* L, int nvb, int kb, int64_
 }
 
 static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, int ct_bytes, PrPart part) {
+  NvtxRange nvtx("gg.pr_block.build_layout");
   const int dev = g.dev;
   const int64_t V = g.V, Eall = g.E;
   if (!g.has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
@@ -721,6 +722,7 @@ struct PrRank {
   // Alg. 2: segments in order, cold first, the hot one last
   Runtime* rt_top = nullptr;  // records the hot-segment launches (dominant kernel)
   void edges(int64_t it, cudaStream_t st) {
+    NvtxRange nvtx("gg.pr_block.edge_phase");
     const CT* c = cur(it);
     for (int64_t k = 1; k <= L->K; ++k) {
       const int64_t sg = k == L->K ? 0 : k;
@@ -762,6 +764,7 @@ struct PrRank {
   // fused all-gather: the peers' contribution buffers (same parity layout)
   std::vector<CT*> peer_c0, peer_c1;
   void vertex(int64_t it, double damping, cudaStream_t st) {
+    NvtxRange nvtx("gg.pr_block.vertex_pass");
     const int64_t lo = L->lo, n = L->vloc();
     PeerSet<CT> ps;
     ps.n = (int)peer_c0.size();
