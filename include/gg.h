@@ -264,9 +264,13 @@ int gg_pagerank_dist(gg_comm* c, const gg_graph* g, int64_t max_iters, double to
 int gg_pagerank_dist_ex(gg_comm* c, const gg_graph* g, const gg_binding* binding,
                         int32_t fp32_contrib, int64_t max_iters, double tolerance, double damping,
                         double* ranks, gg_stats* stats);
-/* Build (and cache) rank `rank` of `nranks`'s layout without running. */
+/* Build (and cache) rank `rank` of `nranks`'s layout without running.
+ * Optionally reports the destination partition (bounds: nranks+1 entries,
+ * in renumbered ids) and the renumbering (newid: V entries, original id ->
+ * renumbered id); both may be NULL (EdgeBlocking schedule only). */
 int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g,
-                             const gg_binding* binding, int32_t fp32_contrib, double* prep_ms);
+                             const gg_binding* binding, int32_t fp32_contrib, double* prep_ms,
+                             int64_t* bounds, int32_t* newid);
 /* Direction-optimizing BFS, 1-D vertex partition (32-aligned, balanced by
  * out-degree), bitmap frontier exchange: top-down levels all-reduce(max)
  * parent candidates, bottom-up levels all-gather the owned next-frontier
@@ -275,6 +279,8 @@ int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g,
  * every rank; a legal BFS tree with the single-GPU depths. */
 int gg_bfs_dist(gg_comm* c, const gg_graph* g, int64_t source, double threshold,
                 int32_t* parents, gg_stats* stats);
+/* The vertex partition gg_bfs_dist uses (nranks+1 entries). */
+int gg_bfs_dist_bounds(const gg_graph* g, int32_t nranks, int64_t* bounds);
 /* The same with `nparts` virtual ranks on the graph's one device (test mode). */
 int gg_bfs_virtual(const gg_graph* g, int32_t nparts, int64_t source, double threshold,
                    int32_t* parents, gg_stats* stats);

@@ -127,7 +127,8 @@ SIGNATURES = {
     "gg_pagerank_dist_ex": (I32, [VP, VP, C.POINTER(GGBinding), I32, I64, F64, F64, VP,
                                   C.POINTER(GGStats)]),
     "gg_pagerank_dist_prepare": (I32, [I32, I32, VP, C.POINTER(GGBinding), I32,
-                                       C.POINTER(F64)]),
+                                       C.POINTER(F64), VP, VP]),
+    "gg_bfs_dist_bounds": (I32, [VP, I32, VP]),
     "gg_bfs_dist": (I32, [VP, VP, I64, F64, VP, C.POINTER(GGStats)]),
     "gg_bfs_virtual": (I32, [VP, I32, I64, F64, VP, C.POINTER(GGStats)]),
     "gg_pagerank_virtual": (I32, [VP, I32, C.POINTER(GGBinding), I32, I32, I64, F64, F64, VP,

@@ -582,7 +582,7 @@ int gg_pagerank_dist_ex(gg_comm* c, const gg_graph* g, const gg_binding* binding
 }
 
 int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g, const gg_binding* binding,
-                             int32_t fp32_contrib, double* prep_ms) {
+                             int32_t fp32_contrib, double* prep_ms, int64_t* bounds, int32_t* newid) {
   GG_API_BEGIN
   NEED(g);
   NEED(binding);
@@ -591,11 +591,12 @@ int gg_pagerank_dist_prepare(int32_t nranks, int32_t rank, const gg_graph* g, co
   DeviceGuard guard(g->g->dev);
   double t0 = now_ms();
   const gg_schedule& s = binding->s1;
-  if (s.load_balance == GG_LB_EDGE_ONLY && s.blocking)
-    pr_block_prep_part_ms(*g->g, s.blocking_size, fp32_contrib ? 4 : 8, nranks, rank);
-  else {
+  if (s.load_balance == GG_LB_EDGE_ONLY && s.blocking) {
+    pr_block_prep_part_ms(*g->g, s.blocking_size, fp32_contrib ? 4 : 8, nranks, rank, bounds, newid);
+  } else {
     g->g->out_view();
     g->g->in_view();
+    if (bounds || newid) fail(GG_ERR_VALUE, "partition bounds are reported for the EdgeBlocking schedule");
   }
   GG_CUDA(cudaDeviceSynchronize());
   if (prep_ms) *prep_ms = now_ms() - t0;
@@ -614,6 +615,17 @@ int gg_bfs_dist(gg_comm* c, const gg_graph* g, int64_t source, double threshold,
   CallTimer t(g->g->dev);
   bfs_dist_run(c, *g->g, source, threshold, parents, rt);
   t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_bfs_dist_bounds(const gg_graph* g, int32_t nranks, int64_t* bounds) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(bounds);
+  if (nranks < 1) fail(GG_ERR_VALUE, "bad nranks");
+  DeviceGuard guard(g->g->dev);
+  std::vector<int64_t> b = bfsd_bounds(*g->g, nranks, 0);
+  memcpy(bounds, b.data(), (nranks + 1) * sizeof(int64_t));
   GG_API_END
 }
 

@@ -29,6 +29,7 @@
 #include "prtile.cuh"  // block_sum
 #include "apply.cuh"
 #include "prdist.cuh"
+#include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/device/device_scan.cuh>
@@ -1015,8 +1016,11 @@ template int64_t pagerank_blocked_rank<double>(const Graph&, const gg_schedule&,
 template int64_t pagerank_blocked_rank<float>(const Graph&, const gg_schedule&, int, int, PrExchange&, int64_t,
                                               double, double, double*, Runtime&, int64_t*);
 
-double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r) {
+double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r,
+                             int64_t* bounds, int32_t* newid) {
   PrBlockLayout* L = layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes, PrPart{P, r});
+  if (bounds) memcpy(bounds, L->bounds.data(), (P + 1) * sizeof(int64_t));
+  if (newid) GG_CUDA(cudaMemcpy(newid, L->newid.p, L->V * sizeof(int32_t), cudaMemcpyDefault));
   return L->prep_ms;
 }
 

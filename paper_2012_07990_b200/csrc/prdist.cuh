@@ -50,6 +50,8 @@ int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r
 template <class CT>
 int64_t pagerank_blocked_virtual(const Graph& g, const gg_schedule& s, int nparts, int64_t max_iters, double tol,
                                  double damping, double* ranks_out, Runtime& rt, bool fused_allgather = false);
-double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r);
+double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r,
+                             int64_t* bounds = nullptr, int32_t* newid = nullptr);
+std::vector<int64_t> bfsd_bounds(const Graph& g, int P, cudaStream_t st);
 
 }  // namespace gg

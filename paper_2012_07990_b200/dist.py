@@ -85,13 +85,64 @@ def pagerank_dist(comm, g, max_iters=100, tolerance=1e-9, damping=0.85, out=None
     return ranks, RunStats.from_pod(st)
 
 
-def prepare_dist(nranks, rank, g, program, contrib_fp32=False):
-    """Build this rank's layout ahead of the timed runs; returns prep ms."""
+def prepare_dist(nranks, rank, g, program, contrib_fp32=False, with_partition=False):
+    """Build this rank's layout ahead of the timed runs; returns prep ms (and,
+    with_partition, the destination bounds in renumbered ids + the
+    renumbering original -> renumbered)."""
     pod = _binding(program)
     ms = C.c_double()
+    bounds = np.empty(nranks + 1, np.int64) if with_partition else None
+    newid = np.empty(g.num_vertices, np.int32) if with_partition else None
     _lib.call("gg_pagerank_dist_prepare", int(nranks), int(rank), g.handle, C.byref(pod),
-              1 if contrib_fp32 else 0, C.byref(ms))
-    return ms.value
+              1 if contrib_fp32 else 0, C.byref(ms), _lib.ptr(bounds), _lib.ptr(newid))
+    return (ms.value, bounds, newid) if with_partition else ms.value
+
+
+def degree_renumbering(num_vertices, src):
+    """Host statement of the EdgeBlocking renumbering (prblock.cu build_layout
+    step 1): vertices by out-degree, descending, ties by id; returns newid."""
+    deg = np.bincount(np.asarray(src, np.int64), minlength=num_vertices)
+    order = np.argsort(-deg, kind="stable")
+    newid = np.empty(num_vertices, np.int64)
+    newid[order] = np.arange(num_vertices)
+    return newid
+
+
+def eb_partition_bounds(num_vertices, src, dst, nranks):
+    """Host statement of the partitioned EdgeBlocking run's destination
+    partition (prblock.cu k_part_bounds): renumbered destinations, balanced
+    by in-edges, bounds rounded down to multiples of 32."""
+    newid = degree_renumbering(num_vertices, src)
+    indeg = np.bincount(newid[np.asarray(dst, np.int64)], minlength=num_vertices)
+    off = np.concatenate(([0], np.cumsum(indeg)))
+    E = int(off[-1])
+    b = [0]
+    for r in range(1, nranks):
+        target = (E * r) // nranks
+        b.append(int(np.searchsorted(off[:num_vertices], target, side="left")) & ~31)
+    b.append(num_vertices)
+    return b
+
+
+def bfs_partition_bounds(out_offsets, nranks):
+    """Host statement of the partitioned BFS's vertex partition (bfsdist.cu
+    k_bfsd_bounds): balanced by out-degree, rounded down to multiples of 32."""
+    off = np.asarray(out_offsets, dtype=np.int64)
+    V = len(off) - 1
+    E = int(off[-1])
+    b = [0]
+    for r in range(1, nranks):
+        target = (E * r) // nranks
+        b.append(int(np.searchsorted(off[:V], target, side="left")) & ~31)
+    b.append(V)
+    return b
+
+
+def bfs_dist_bounds(g, nranks):
+    """The device's BFS vertex partition (gg_bfs_dist_bounds)."""
+    b = np.empty(nranks + 1, np.int64)
+    _lib.call("gg_bfs_dist_bounds", g.handle, int(nranks), _lib.ptr(b))
+    return b.tolist()
 
 
 def pagerank_virtual(g, nparts, program, max_iters=100, tolerance=1e-9, damping=0.85,

@@ -120,3 +120,20 @@ def test_bfs_dist_single_rank_matches_oracle():
     parents, st = bfs_dist(comm, g, src, 0.05)
     _levels_and_tree(gg, g, parents, src, off, nbr)
     comm.close()
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_device_partitions_equal_host_statements(nranks):
+    """The device's partitions (EdgeBlocking destinations in renumbered ids,
+    BFS vertices) equal the host statements in dist.py."""
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200 import dist
+    V, s, d = gen.rmat(12, 16, seed=5)
+    g = gg.Graph.from_coo(V, s, d)
+    for r in (0, nranks - 1):
+        _, bounds, newid = dist.prepare_dist(nranks, r, g, _eb_program(gg), with_partition=True)
+        assert bounds.tolist() == dist.eb_partition_bounds(V, s, d, nranks)
+        assert np.array_equal(newid, dist.degree_renumbering(V, s))
+    gs = gg.generate_rmat(11, 8, seed=3, symmetrize=True)
+    off = np.asarray(gs.out_offsets, np.int64)
+    assert dist.bfs_dist_bounds(gs, nranks) == dist.bfs_partition_bounds(off, nranks)
