@@ -119,9 +119,23 @@ struct OutBuilder {
       return true;
     }
     if (mode == GG_CREATE_UNFUSED_BITMAP) {
-      if (dedup == DEDUP_SLOT) return !test_and_set_bit(bits, v);
-      if (dedup != DEDUP_NONE && !accept(v)) return false;
-      atomicOr(bits + (v >> 5), 1u << (v & 31));
+      if (dedup != DEDUP_SLOT && dedup != DEDUP_NONE && !accept(v)) return false;
+      // warp-aggregated bit set: lanes whose vertices share an output word
+      // OR their bits together and one of them issues the atomic (a pull
+      // level sets 32 consecutive vertices' bits from one warp); with slot
+      // dedup the first lane holding a vertex takes it iff its bit was clear
+      const unsigned act = __activemask();
+      const unsigned lane = lane_id();
+      const unsigned same_v = __match_any_sync(act, v);
+      const bool first_v = lane == (unsigned)(__ffs(same_v) - 1);
+      const uint32_t w = (uint32_t)v >> 5, bit = 1u << (v & 31);
+      const unsigned same_w = __match_any_sync(act, w);
+      const uint32_t m = __reduce_or_sync(same_w, first_v ? bit : 0u);
+      const int leader = __ffs(same_w) - 1;
+      uint32_t old = 0;
+      if ((int)lane == leader) old = atomicOr(bits + w, m);
+      old = __shfl_sync(same_w, old, leader);
+      if (dedup == DEDUP_SLOT) return first_v && !(old & bit);
       return true;
     }
     return false;
