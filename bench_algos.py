@@ -156,7 +156,7 @@ def sssp_c3(gg, args, peak):
 def cc_bc_c4(gg, args, peak):
     scale = args.scale or 25
     t0 = time.perf_counter()
-    g = gg.generate_kronecker(scale, 16, seed=5, symmetrize=True)
+    g = gg.generate_kronecker(scale, 16, seed=5, symmetrize=True, sort_by_source=True)
     gen_s = time.perf_counter() - t0
     V, A = g.num_vertices, g.num_edges
     deg = np.diff(np.asarray(g.out_offsets, dtype=np.int64))
@@ -221,6 +221,7 @@ def cc_bc_c4(gg, args, peak):
     ms = cc_res[head]["ms"]
     return {"value": cc_res[head]["gteps"], "ms_per_step": ms, "steps": max(1, args.steps),
             "config": {"workload": "cc_bc_kron%d_ef16_sym" % scale, "V": V, "arcs": A,
+                       "coo_order": "by source (edge-list order; matters for EDGE_ONLY/EB only)",
                        "headline": "CC %s (GTEPS = A x hooking rounds / time)" % head,
                        "cc": cc_res, "bc": bc_res, "bc_sources": bc_sources,
                        "bc_m_c": m_c, "generate_s": gen_s},

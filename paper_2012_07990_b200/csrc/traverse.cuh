@@ -921,6 +921,7 @@ struct EdgeArgs {
   Op op;
   OutBuilder out;
   int use_filter;
+  int batch4 = 1;  // GG_EDGE_BATCH4=0 turns the four-arc path off (A/B)
 };
 
 template <class Op>
@@ -944,7 +945,7 @@ __device__ __forceinline__ void edge_range(const EdgeArgs<Op>& a, int64_t lo, in
   const int4* s4 = reinterpret_cast<const int4*>(a.coo.src + head);
   const int4* d4 = reinterpret_cast<const int4*>(a.coo.dst + head);
   if constexpr (PushBatch4<Op>::value) {
-    if (a.in.repr == -1 && !a.use_filter) {  // every source active, no filter
+    if (a.batch4 && a.in.repr == -1 && !a.use_filter) {  // every source active, no filter
       for (int64_t k = tid; k < nvec; k += nthreads) {
         const int4 s = ld_stream4(s4 + k), d = ld_stream4(d4 + k);
         a.op.push4(s, d);

@@ -330,8 +330,10 @@ def generate_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, symmetr
     return _generate(GEN_RMAT, scale, edge_factor, a, b, c, seed, flags, device)
 
 
-def generate_kronecker(scale, edge_factor=16, seed=5, symmetrize=True, weights=False, device=0):
-    flags = (F_SYMMETRIZE if symmetrize else 0) | (F_WEIGHTS if weights else 0)
+def generate_kronecker(scale, edge_factor=16, seed=5, symmetrize=True, weights=False,
+                       sort_by_source=False, device=0):
+    flags = ((F_SYMMETRIZE if symmetrize else 0) | (F_WEIGHTS if weights else 0)
+             | (F_SORT_BY_SOURCE if sort_by_source else 0))
     return _generate(GEN_KRON, scale, edge_factor, 0.57, 0.19, 0.19, seed, flags, device)
 
 
