@@ -121,7 +121,6 @@ void run_edge_only(Runtime* rt, const gg_schedule& s, const Op& op, bool use_fil
   const int dev = rt->dev;
   if (!g->has_coo) fail(GG_ERR_ENGINE, "graph COO view was dropped");
   EdgeArgs<Op> a{g->coo_view(), in, op, out, use_filter ? 1 : 0};
-  if (const char* e = getenv("GG_EDGE_BATCH4")) a.batch4 = atoi(e) != 0;
   if (s.blocking) {
     int64_t n = s.blocking_size > 0 ? s.blocking_size : default_blocking_size(*g);
     Blocked* b = blocked_for(*const_cast<Graph*>(g), n);

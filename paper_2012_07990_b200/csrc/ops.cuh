@@ -126,32 +126,6 @@ struct OpHook {
   __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
     hook(u, v);
   }
-  // four arcs at once (EDGE_ONLY streams, traverse.cuh PushBatch4): the
-  // eight label reads, then the four root reads, are issued together,
-  // through L1.  A label read early or from L1 is at most stale (labels only
-  // decrease, the atomicMin acts on the current value), which Soman hooking
-  // tolerates: the round repeats until no hook changes a label.
-  static constexpr bool kPushBatch4 = true;
-  __device__ __forceinline__ void push4(int4 u, int4 v) const {
-    const int32_t us[4] = {u.x, u.y, u.z, u.w}, vs[4] = {v.x, v.y, v.z, v.w};
-    int32_t la[4], lb[4], lo[4], hi[4], lh[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      la[k] = __ldca(label + us[k]);  // L1-cached: runs of one source hit
-      lb[k] = __ldca(label + vs[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      lo[k] = la[k] < lb[k] ? la[k] : lb[k];
-      hi[k] = la[k] < lb[k] ? lb[k] : la[k];
-      lh[k] = la[k] != lb[k] ? __ldca(label + hi[k]) : lo[k];
-    }
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (lo[k] < lh[k] && atomicMin(label + hi[k], lo[k]) > lo[k]) any = true;
-    if (any && !*((volatile int*)changed)) *changed = 1;
-  }
   __device__ __forceinline__ Acc init() const { return 0; }
   __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t) const {
     hook(u, v);

@@ -459,14 +459,6 @@ struct EtwcEntry {
 // slice of the active list): such ranges are handed to the whole grid.
 constexpr int64_t kEtwcHuge = 16384;
 
-// Ops that can take four arcs at once (kPushBatch4 + push4): their loads
-// for the four arcs are issued together instead of one arc's dependent chain
-// after another (CC hook: eight label reads, then the hooks).
-template <class, class = void>
-struct PushBatch4 : std::false_type {};
-template <class T>
-struct PushBatch4<T, std::void_t<decltype(T::kPushBatch4)>> : std::integral_constant<bool, T::kPushBatch4> {};
-
 // Ops whose push is "accumulate into the SOURCE" (BC backward: delta[u] +=
 // f(v)) declare kPushReduce and provide push_val / push_commit: a range walk
 // sums its arcs per thread, reduces over the warp and issues one atomic per
@@ -501,12 +493,6 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
     int32_t v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = __ldg(a.g.nbr + e + k * stride);
-    if constexpr (PushBatch4<Op>::value) {
-      if (!a.use_filter) {
-        a.op.push4(make_int4(u, u, u, u), make_int4(v[0], v[1], v[2], v[3]));
-        continue;
-      }
-    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (a.use_filter && !a.op.filter(v[k])) continue;
@@ -921,7 +907,6 @@ struct EdgeArgs {
   Op op;
   OutBuilder out;
   int use_filter;
-  int batch4 = 1;  // GG_EDGE_BATCH4=0 turns the four-arc path off (A/B)
 };
 
 template <class Op>
@@ -944,15 +929,6 @@ __device__ __forceinline__ void edge_range(const EdgeArgs<Op>& a, int64_t lo, in
   int64_t nvec = (hi - head) >> 2;
   const int4* s4 = reinterpret_cast<const int4*>(a.coo.src + head);
   const int4* d4 = reinterpret_cast<const int4*>(a.coo.dst + head);
-  if constexpr (PushBatch4<Op>::value) {
-    if (a.batch4 && a.in.repr == -1 && !a.use_filter) {  // every source active, no filter
-      for (int64_t k = tid; k < nvec; k += nthreads) {
-        const int4 s = ld_stream4(s4 + k), d = ld_stream4(d4 + k);
-        a.op.push4(s, d);
-      }
-      nvec = 0;
-    }
-  }
   for (int64_t k = tid; k < nvec; k += nthreads) {
     int4 s = ld_stream4(s4 + k), d = ld_stream4(d4 + k);
     int64_t e = head + 4 * k;
