@@ -72,7 +72,7 @@ def parse():
     p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")
     p.add_argument("--lb", default="WM", help="c3 load balance (swept: WM best)")
     p.add_argument("--no-fusion", action="store_true", help="c3: unfused loop")
-    p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED,EB,HYBRID",
+    p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED,EB,EDGE,HYBRID",
                    help="c4 load balances (EB = EDGE_ONLY+BLOCKED, EDGE = EDGE_ONLY)")
     p.add_argument("--check", action="store_true", help="c2-c4: validate against the oracle")
     return p.parse_args()
