@@ -357,7 +357,11 @@ __device__ __forceinline__ void pr_load_edges(const int32_t* __restrict__ src, c
   }
 }
 
-// Gather + reduce one warp step (kE*32 edges).  Runs of equal destination
+// Gather + reduce one warp step (kE*32 edges).  Invariant: destinations are
+// nondecreasing over [e0, e1) (one segment), so equal destinations are
+// contiguous across lanes -- the segmented scan relies on it (a launch over
+// several segments would break it: measured and rejected, it was also
+// slower).  Runs of equal destination
 // inside a lane are summed in registers; runs crossing lanes are joined by ONE
 // warp segmented scan per step; each destination run issues one f64 add.
 // kSmem: sources < nhot are read from the CTA's shared-memory copy of the
@@ -634,7 +638,6 @@ struct HotCfg {
   int32_t nhot = 0;
   int per_sm = 1;
   bool prefetch = true;
-  bool merge_cold = false;
   int gather = 0;
   unsigned grid = 0, hot_grid = 0;
 };
@@ -669,8 +672,6 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
   }
   const char* pf_env = getenv("GG_PR_PREFETCH");
   h.prefetch = !(pf_env && atoi(pf_env) == 0);
-  const char* mc_env = getenv("GG_PR_MERGE_COLD");
-  h.merge_cold = mc_env && atoi(mc_env) != 0;
   if (const char* ge = getenv("GG_PR_GATHER")) h.gather = std::max(0, std::min(2, atoi(ge)));
   if (h.nhot && h.per_sm == 1 && h.gather) {
     const void* fn = h.gather == 1 ? (const void*)k_pr_edges_hot<CT, 1024, 1, 1> : (const void*)k_pr_edges_hot<CT, 1024, 1, 2>;
@@ -728,23 +729,8 @@ struct PrRank {
   void edges(int64_t it, cudaStream_t st) {
     NvtxRange nvtx("gg.pr_block.edge_phase");
     const CT* c = cur(it);
-    // the cold segments are contiguous in the blocked arrays: with
-    // hc.merge_cold they run as ONE launch whose warps stride through them in
-    // order (segment windows still stream through L2 one after the other,
-    // without a launch tail per segment); else one launch per segment
-    if (hc.merge_cold && L->K > 2) {
-      const int64_t e0 = L->seg_edge[1], e1 = L->seg_edge[L->K];
-      if (e1 > e0) {
-        if (hc.prefetch)
-          k_pr_edges<CT, true><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
-        else
-          k_pr_edges<CT, false><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
-        ++launches;
-      }
-    }
     for (int64_t k = 1; k <= L->K; ++k) {
       const int64_t sg = k == L->K ? 0 : k;
-      if (sg != 0 && hc.merge_cold && L->K > 2) continue;
       const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
       if (e1 <= e0) continue;
       cudaEvent_t ta = nullptr, tb = nullptr;
