@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from .frontier import VertexSubset, _ForeignSubset
 from .runtime import EngineError, ExecConfig, RunStats, Runtime, coerce_runtime
-from .sched import (PULL, PUSH, HybridSchedule, Schedule, ScheduleError, validate,
+from .sched import (PULL, HybridSchedule, Schedule, ScheduleError, validate,
                     validate_hybrid, DIRECTION_CODE, LB_CODE, CREATION_CODE, DEDUP_CODE,
                     REPR_CODE)
 from .udfs import DeviceFilter, DeviceUDF
