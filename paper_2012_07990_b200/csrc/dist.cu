@@ -153,7 +153,6 @@ struct NcclExchange : PrExchange {
   gg_comm* c;
   std::vector<void*> opened;  // IPC-mapped peer buffers (closed by unmap_peers)
   explicit NcclExchange(gg_comm* cc) : c(cc) {}
-  ~NcclExchange() override { unmap_peers(); }
   // Fused all-gather over NVLink: every rank exports its two contribution
   // buffers (cudaIpcGetMemHandle), the handles are all-gathered over NCCL,
   // and each peer's buffers are mapped (cudaIpcOpenMemHandle).  Enabled by
@@ -243,6 +242,44 @@ struct NcclExchange : PrExchange {
       if (cnt) GG_NCCL(api.Broadcast(p, p, cnt, ncclUint8, r, c->comm, st));
     }
     GG_NCCL(api.GroupEnd());
+  }
+  // overlap: the rest of the all-gather runs on a non-blocking side stream
+  // (it does not serialise with the legacy default stream the kernels use)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  bool pending = false;
+  void allgather_split(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                       int64_t hot_end, cudaStream_t st) override {
+    std::vector<int64_t> hb(bounds.size()), cb(bounds.size());
+    split_bounds(bounds, hot_end, hb, cb);
+    if (!side) {
+      GG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      GG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      GG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    }
+    allgather(bufs, elt, hb, st);
+    // the rest starts only after the hot part: collectives on one
+    // communicator must run in the same order on every rank, so two of them
+    // may never be in flight at once from different streams (the main
+    // stream's next collective waits for `done` via wait_rest)
+    GG_CUDA(cudaEventRecord(ready, st));
+    GG_CUDA(cudaStreamWaitEvent(side, ready, 0));
+    allgather(bufs, elt, cb, side);
+    GG_CUDA(cudaEventRecord(done, side));
+    pending = true;
+  }
+  void wait_rest(cudaStream_t st) override {
+    if (pending) GG_CUDA(cudaStreamWaitEvent(st, done, 0));
+    pending = false;
+  }
+  ~NcclExchange() override {
+    unmap_peers();
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+      cudaEventDestroy(ready);
+      cudaEventDestroy(done);
+    }
   }
 };
 

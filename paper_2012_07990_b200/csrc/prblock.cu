@@ -726,11 +726,14 @@ struct PrRank {
   CT* nxt(int64_t it) const { return (it & 1) ? c0 : c1; }
   // Alg. 2: segments in order, cold first, the hot one last
   Runtime* rt_top = nullptr;  // records the hot-segment launches (dominant kernel)
-  void edges(int64_t it, cudaStream_t st) {
+  // which: 0 = every segment (cold ones first, the hot one last),
+  //        1 = only the hot segment, 2 = only the cold segments
+  void edges(int64_t it, cudaStream_t st, int which = 0) {
     NvtxRange nvtx("gg.pr_block.edge_phase");
     const CT* c = cur(it);
     for (int64_t k = 1; k <= L->K; ++k) {
       const int64_t sg = k == L->K ? 0 : k;
+      if ((which == 1 && sg != 0) || (which == 2 && sg == 0)) continue;
       const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
       if (e1 <= e0) continue;
       cudaEvent_t ta = nullptr, tb = nullptr;
@@ -883,9 +886,20 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
       for (void* q : pc0[i]) ranks[i]->peer_c0.push_back(static_cast<CT*>(q));
       for (void* q : pc1[i]) ranks[i]->peer_c1.push_back(static_cast<CT*>(q));
     }
+  // Without the fused all-gather the exchange overlaps the next iteration's
+  // hot kernel: the hot window [0, ns) of every slice is gathered first (it
+  // is small and all the hot kernel reads), the rest asynchronously; the
+  // cold segments wait for it.  Hot first, cold after: acc sums commute.
+  const bool split = !p2p && L0->P > 1;
   while (!(it >= max_iters || l1 < tol)) {
     rt.edge_begin();
-    for (auto* R : ranks) R->edges(it, st);
+    if (split) {
+      for (auto* R : ranks) R->edges(it, st, 1);
+      ex.wait_rest(st);
+      for (auto* R : ranks) R->edges(it, st, 2);
+    } else {
+      for (auto* R : ranks) R->edges(it, st);
+    }
     rt.edge_end();
     for (size_t i = 0; i < ranks.size(); ++i) {
       ranks[i]->vertex(it, damping, st);
@@ -893,7 +907,10 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
       nx[i] = ranks[i]->nxt(it);
     }
     ex.allreduce2(sc, st);  // also the barrier after which peer stores are visible
-    if (!p2p) ex.allgather(nx, sizeof(CT), L0->bounds, st);
+    if (split)
+      ex.allgather_split(nx, sizeof(CT), L0->bounds, L0->ns, st);
+    else if (!p2p)
+      ex.allgather(nx, sizeof(CT), L0->bounds, st);
     rt.stats.dispatch_count += 1;
     rt.stats.direction_log.push_back(direction_log);
     ++it;
@@ -910,6 +927,7 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
     }
     ex.unmap_peers();
   }
+  if (split) ex.wait_rest(st);  // the last iteration's contributions: nobody reads them
   // every rank's owned rank slice to all ranks
   std::vector<void*> rk(ranks.size());
   for (size_t i = 0; i < ranks.size(); ++i) rk[i] = ranks[i]->rank;

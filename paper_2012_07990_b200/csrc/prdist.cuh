@@ -28,6 +28,26 @@ struct PrExchange {
     return false;
   }
   virtual void unmap_peers() {}
+  // Split all-gather for overlap: the part of every slice below hot_end
+  // (the hot source window the next iteration's first kernel gathers from)
+  // on the main stream, the rest started asynchronously; wait_rest(st) makes
+  // the main stream wait for it.  Default: everything on the main stream.
+  virtual void allgather_split(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
+                               int64_t hot_end, cudaStream_t st) {
+    std::vector<int64_t> hb(bounds.size()), cb(bounds.size());
+    split_bounds(bounds, hot_end, hb, cb);
+    allgather(bufs, elt, hb, st);
+    allgather(bufs, elt, cb, st);
+  }
+  virtual void wait_rest(cudaStream_t) {}
+  // each slice [b_r, b_r+1) cut at h: [min(b_r,h), min(b_r+1,h)) and [max(b_r,h), max(b_r+1,h))
+  static void split_bounds(const std::vector<int64_t>& b, int64_t h, std::vector<int64_t>& hot,
+                           std::vector<int64_t>& rest) {
+    for (size_t i = 0; i < b.size(); ++i) {
+      hot[i] = b[i] < h ? b[i] : h;
+      rest[i] = b[i] > h ? b[i] : h;
+    }
+  }
 };
 
 // Exchange of the partitioned BFS (bfsdist.cu): an element-wise max of an
