@@ -389,10 +389,7 @@ __device__ __forceinline__ float ld_gather(const float* p) {
   return __ldg(p);
 }
 
-// kB: lanes per scan block.  32 = one segmented scan over the warp (5
-// shuffle steps); 8 = independent 8-lane blocks (3 steps), a run crossing a
-// block boundary emits one add per block it touches (GG_PR_SCAN_BLOCK).
-template <class CT, bool kSmem, int kLoad = 0, int kB = 32>
+template <class CT, bool kSmem, int kLoad = 0>
 __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const int32_t (&dv)[kE], const CT* contrib,
                                                double* acc, int coherent, const CT* s_hot, int32_t nhot) {
   const int lane = lane_id();
@@ -430,29 +427,28 @@ __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const in
   int td = run_d;
   double tv = run;
 #pragma unroll
-  for (int o = 1; o < kB; o <<= 1) {
+  for (int o = 1; o < 32; o <<= 1) {
     double t = __shfl_up_sync(0xffffffffu, tv, o);
     int dd = __shfl_up_sync(0xffffffffu, td, o);
-    if ((lane & (kB - 1)) >= o && dd == td) tv += t;
+    if (lane >= o && dd == td) tv += t;
   }
   const int prev_td = __shfl_up_sync(0xffffffffu, td, 1);
   const double prev_tv = __shfl_up_sync(0xffffffffu, tv, 1);
   const int next_head = __shfl_down_sync(0xffffffffu, head_d, 1);
-  const bool block_first = (lane & (kB - 1)) == 0, block_last = (lane & (kB - 1)) == kB - 1;
   if (has_head && head_d >= 0) {
     double h = head;
-    if (!block_first && prev_td == head_d) h += prev_tv;  // a block end emitted its own
+    if (lane > 0 && prev_td == head_d) h += prev_tv;
     atomicAdd(acc + head_d, h);
   }
-  // my tail is emitted by me unless the next lane (same block) continues it
-  if (td >= 0 && (block_last || next_head != td)) atomicAdd(acc + td, tv);
+  // my tail is emitted by me unless the next lane continues it
+  if (td >= 0 && (lane == 31 || next_head != td)) atomicAdd(acc + td, tv);
 }
 
 // Edge phase (EDGE_ONLY semantics, Alg. 2) over blocked edges [e0, e1) of one
 // segment: warps stride over kE*32-edge steps; the next step's edges are
 // loaded (registers) before the current step's gathers, so the DRAM latency
 // of the edge stream overlaps the L2 latency of the gathers.
-template <class CT, bool kSmem = false, bool kPrefetch = true, int kLoad = 0, int kB = 32>
+template <class CT, bool kSmem = false, bool kPrefetch = true, int kLoad = 0>
 __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                              int64_t e0, int64_t e1, const CT* contrib, double* acc,
                                              int coherent, const CT* s_hot = nullptr, int32_t nhot = 0) {
@@ -468,12 +464,12 @@ __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, co
   for (; base < e1; base += stride) {
     if (!kPrefetch) {
       if (base != start + warp * 32 * kE) pr_load_edges(src, dst, base + lane * kE, e0, e1, su, dv);
-      pr_reduce_step<CT, kSmem, kLoad, kB>(su, dv, contrib, acc, coherent, s_hot, nhot);
+      pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot);
       continue;
     }
     int32_t nsu[kE], ndv[kE];
     pr_load_edges(src, dst, base + stride + lane * kE, e0, e1, nsu, ndv);  // dead past e1
-    pr_reduce_step<CT, kSmem, kLoad, kB>(su, dv, contrib, acc, coherent, s_hot, nhot);
+    pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot);
 #pragma unroll
     for (int q = 0; q < kE; ++q) {
       su[q] = nsu[q];
@@ -492,7 +488,7 @@ static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, con
 // are staged once per CTA in shared memory; their gathers leave the L1TEX
 // line pipeline and the L2 (the two bounds of this kernel, ~1 line/clk/SM)
 // for the shared-memory banks.
-template <class CT, int kThreads, int kMinBlocks, int kLoad = 0, int kB = 32>
+template <class CT, int kThreads, int kMinBlocks, int kLoad = 0>
 static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(const int32_t* src, const int32_t* dst,
                                                                              int64_t e0, int64_t e1, const CT* contrib,
                                                                              double* acc, int32_t nhot) {
@@ -503,7 +499,7 @@ static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(co
     reinterpret_cast<int4*>(s_raw)[i] = __ldg(reinterpret_cast<const int4*>(contrib) + i);
   for (int i = n4 * (16 / (int)sizeof(CT)) + threadIdx.x; i < nhot; i += blockDim.x) s_hot[i] = __ldg(contrib + i);
   __syncthreads();
-  pr_edges_seg<CT, true, true, kLoad, kB>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
+  pr_edges_seg<CT, true, true, kLoad>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
 }
 
 // Peer contribution buffers of a partitioned run with the fused all-gather:
@@ -643,7 +639,6 @@ struct HotCfg {
   int per_sm = 1;
   bool prefetch = true;
   int gather = 0;
-  int scan_block = 32;
   unsigned grid = 0, hot_grid = 0;
 };
 
@@ -678,12 +673,6 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
   const char* pf_env = getenv("GG_PR_PREFETCH");
   h.prefetch = !(pf_env && atoi(pf_env) == 0);
   if (const char* ge = getenv("GG_PR_GATHER")) h.gather = std::max(0, std::min(2, atoi(ge)));
-  if (const char* sb = getenv("GG_PR_SCAN_BLOCK")) h.scan_block = atoi(sb) == 8 ? 8 : (atoi(sb) == 16 ? 16 : 32);
-  if (h.nhot && h.per_sm == 1 && h.scan_block != 32) {
-    const void* fn = h.scan_block == 8 ? (const void*)k_pr_edges_hot<CT, 1024, 1, 0, 8>
-                                       : (const void*)k_pr_edges_hot<CT, 1024, 1, 0, 16>;
-    GG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
-  }
   if (h.nhot && h.per_sm == 1 && h.gather) {
     const void* fn = h.gather == 1 ? (const void*)k_pr_edges_hot<CT, 1024, 1, 1> : (const void*)k_pr_edges_hot<CT, 1024, 1, 2>;
     GG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
@@ -763,12 +752,6 @@ struct PrRank {
       else if (sg == 0 && hc.nhot > 0 && hc.gather == 2)
         k_pr_edges_hot<CT, 1024, 1, 2><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
                                                                                        e1, c, acc, hc.nhot);
-      else if (sg == 0 && hc.nhot > 0 && hc.scan_block == 8)
-        k_pr_edges_hot<CT, 1024, 1, 0, 8><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
-                                                                                          e1, c, acc, hc.nhot);
-      else if (sg == 0 && hc.nhot > 0 && hc.scan_block == 16)
-        k_pr_edges_hot<CT, 1024, 1, 0, 16><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
-                                                                                           e1, c, acc, hc.nhot);
       else if (sg == 0 && hc.nhot > 0)
         k_pr_edges_hot<CT, 1024, 1><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1,
                                                                                     c, acc, hc.nhot);
