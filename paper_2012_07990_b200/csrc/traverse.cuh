@@ -651,6 +651,7 @@ __device__ __forceinline__ void b_pull_vb(PullArgs<Op> a) {
         acc = Op::warp_reduce(acc);
         if (lane == 0) a.op.finish(u, acc, a.out);
       }
+      __syncthreads();  // every warp is done with s_long / s_nlong before the reset
     }
     add_scanned(a.scanned, sc);
     return;

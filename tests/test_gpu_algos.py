@@ -342,3 +342,25 @@ def test_scale16_bc_vs_reference(gg, s16, lb):
     assert g.num_edges == int(s16["bc_arcs"])
     r = gg.bc(g, [int(x) for x in s16["bc_sources"]], program_with(gg.Schedule(load_balance=lb)))
     close_bc(r.array, s16["bc_scores"])
+
+
+@pytest.mark.parametrize("sch", ["PULL-VERTEX_BASED", "HYBRID"])
+def test_bfs_more_vertices_than_grid_threads(gg, sch):
+    """V > grid threads (1184 x 256 on B200): grid-stride loops run several
+    tiles per CTA (the two-phase bottom-up kernel re-arms its shared queue
+    between tiles), levels bit-exact vs the oracle."""
+    g = gg.generate_rmat(19, 8, seed=21, symmetrize=True)
+    V = g.num_vertices
+    off = np.asarray(g.out_offsets, np.int64)
+    nbr = np.asarray(g.out_neighbors, np.int32)
+    if sch == "HYBRID":
+        prog = gg.ScheduleProgram({"s0:s1": gg.HybridSchedule(
+            threshold=0.001, s1=gg.Schedule(direction="PUSH", load_balance="ETWC", dedup=False),
+            s2=gg.Schedule(direction="PULL", pull_frontier_repr="BITMAP",
+                           frontier_creation="UNFUSED_BITMAP"))})
+    else:
+        prog = program_with(gg.Schedule(direction="PULL", load_balance="VERTEX_BASED"))
+    for src in (int(np.argmax(np.diff(off))), 12345):
+        r = gg.bfs(g, src, prog)
+        assert np.array_equal(np.asarray(gg.bfs_levels(r.array)),
+                              oracle.bfs_levels(V, off, nbr, src, parallel=True))
