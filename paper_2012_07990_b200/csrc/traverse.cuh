@@ -610,52 +610,11 @@ __device__ __forceinline__ bool pull_visit(const PullArgs<Op>& a, typename Op::A
 }
 
 // VERTEX_BASED: thread per destination (early exit when the op says so).
-// Early-exit ops (BFS bottom-up) run in two phases per CTA tile of 256
-// destinations: every thread probes its destination's first kProbe
-// in-arcs (most settle on the first: hubs come first in the sorted in-lists
-// and sit in the frontier); the unsettled ones are queued in shared memory
-// and scanned warp-cooperatively, 32 in-arcs per step with a ballot exit --
-// instead of long per-thread scans that idle the rest of the warp.
-constexpr int kProbe = 2;
+// (A two-phase variant -- per-thread probe of the first two in-arcs, then
+// warp-cooperative scans of the unsettled destinations -- measured 3x slower
+// on the first RMAT-24 bottom-up level: 1.52 vs 0.52 ms.)
 template <class Op>
 __device__ __forceinline__ void b_pull_vb(PullArgs<Op> a) {
-  if constexpr (Op::kEarlyExit) {
-    __shared__ int32_t s_long[256];
-    __shared__ int s_nlong;
-    int64_t sc = 0;
-    const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < a.g.V;
-         base += (int64_t)gridDim.x * blockDim.x) {
-      if (threadIdx.x == 0) s_nlong = 0;
-      __syncthreads();
-      const int64_t v = base + threadIdx.x;
-      if (v < a.g.V && (!a.use_filter || a.op.filter((int32_t)v))) {
-        const int64_t lo = __ldg(a.g.off + v), hi = __ldg(a.g.off + v + 1);
-        sc += hi - lo;
-        typename Op::Acc acc = a.op.init();
-        bool done = false;
-        for (int64_t e = lo; e < hi && e < lo + kProbe; ++e)
-          if (pull_visit(a, acc, (int32_t)v, e)) { done = true; break; }
-        if (done || hi - lo <= kProbe) a.op.finish((int32_t)v, acc, a.out);
-        else s_long[atomicAdd(&s_nlong, 1)] = (int32_t)v;
-      }
-      __syncthreads();
-      for (int k = wid; k < s_nlong; k += nw) {
-        const int32_t u = s_long[k];
-        const int64_t lo = __ldg(a.g.off + u) + kProbe, hi = __ldg(a.g.off + u + 1);
-        typename Op::Acc acc = a.op.init();
-        for (int64_t e0 = lo; e0 < hi; e0 += kWarp) {
-          const bool stop = e0 + lane < hi && pull_visit(a, acc, u, e0 + lane);
-          if (__any_sync(0xffffffffu, stop)) break;
-        }
-        acc = Op::warp_reduce(acc);
-        if (lane == 0) a.op.finish(u, acc, a.out);
-      }
-      __syncthreads();  // every warp is done with s_long / s_nlong before the reset
-    }
-    add_scanned(a.scanned, sc);
-    return;
-  }
   int64_t sc = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < a.g.V;
        v += (int64_t)gridDim.x * blockDim.x) {
