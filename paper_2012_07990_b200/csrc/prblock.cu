@@ -45,7 +45,7 @@ struct PrPart {
 };
 
 struct PrBlockLayout {
-  int64_t ns = 0, K = 0, V = 0, E = 0;
+  int64_t ns = 0, ns_cold = 0, K = 0, V = 0, E = 0;  // hot window, cold windows
   int ct_bytes = 0;
   int P = 1, r = 0;
   int64_t lo = 0, hi = 0;                            // owned destinations (renumbered ids)
@@ -99,7 +99,8 @@ __global__ void k_relabel_tables(const int32_t* order, const uint32_t* deg, int6
 // edges whose destination another rank owns get segment K (sorted last).
 template <class KT>
 __global__ void k_edge_keys(const int32_t* s, const int32_t* d, int64_t E, const int32_t* newid,
-                            int64_t ns, int nvb, int64_t lo, int64_t hi, uint64_t K, KT* key, int32_t* val) {
+                            int64_t ns, int64_t ns_cold, int nvb, int64_t lo, int64_t hi, uint64_t K, KT* key,
+                            int32_t* val) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t nu = newid[s[e]];
@@ -109,7 +110,9 @@ __global__ void k_edge_keys(const int32_t* s, const int32_t* d, int64_t E, const
       key[e] = (KT)(K << nvb);
       continue;
     }
-    key[e] = (KT)((((uint64_t)nu / (uint64_t)ns) << nvb) | (uint64_t)(nv - lo));
+    // segment 0 = the hot window [0, ns); then cold windows of ns_cold sources
+    const uint64_t seg = (uint64_t)nu < (uint64_t)ns ? 0 : 1 + ((uint64_t)nu - ns) / (uint64_t)ns_cold;
+    key[e] = (KT)((seg << nvb) | (uint64_t)(nv - lo));
   }
 }
 template <class KT>
@@ -180,7 +183,8 @@ static void sort_edges(const Graph& g, PrBlockLayout* L, int nvb, int kb, int64_
     DevBuf<KT> k0(Eall);
     DevBuf<int32_t> v0(Eall);
     L->src.alloc(Eall);  // payload: renumbered sources in (segment, destination) order
-    k_edge_keys<KT><<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, Eall, L->newid.p, L->ns, nvb,
+    k_edge_keys<KT><<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, Eall, L->newid.p, L->ns,
+                                                       L->ns_cold, nvb,
                                                        L->lo, L->hi, (uint64_t)L->K, k0.p, v0.p);
     GG_LAUNCH_CHECK();
     size_t temp = 0;
@@ -207,7 +211,11 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   auto L = std::make_shared<PrBlockLayout>();
   double t0 = now_ms();
   L->ns = ns;
-  L->K = (V + ns - 1) / ns;
+  // cold windows: GG_PR_COLD_WINDOW16 sixteenths of L2 (default: the hot size)
+  L->ns_cold = ns;
+  if (const char* e = getenv("GG_PR_COLD_WINDOW16"))
+    L->ns_cold = std::max<int64_t>(ns, l2_bytes(g.dev) * std::max(1, atoi(e)) / 16 / ct_bytes);
+  L->K = V > ns ? 1 + (V - ns + L->ns_cold - 1) / L->ns_cold : 1;
   L->V = V;
   L->ct_bytes = ct_bytes;
   L->P = part.P;
