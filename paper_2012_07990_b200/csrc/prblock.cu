@@ -524,15 +524,17 @@ struct PeerSet {
 // vertex pass: rank' = base + d*acc, L1, next dangling mass, next contrib, acc reset.
 // 4 consecutive vertices per thread with 16-byte loads/stores (restrict ->
 // all loads of a group are issued before any store).
-template <class CT>
+template <class CT, bool kRank = true>
 __device__ __forceinline__ void pr_vertex_one(int64_t v, const int32_t* __restrict__ outdeg,
                                               double* __restrict__ rank, CT* __restrict__ contrib_next,
                                               double* __restrict__ acc, double base, double damping,
                                               double& l1, double& dm, const PeerSet<CT>& peers) {
   const double nv = base + damping * acc[v];
   acc[v] = 0.0;
-  l1 += fabs(nv - rank[v]);
-  rank[v] = nv;
+  if (kRank) {
+    l1 += fabs(nv - rank[v]);
+    rank[v] = nv;
+  }
   const int32_t od = outdeg[v];
   if (od) {
     const CT c = (CT)(nv / (double)od);
@@ -543,7 +545,12 @@ __device__ __forceinline__ void pr_vertex_one(int64_t v, const int32_t* __restri
   }
 }
 
-template <class CT>
+// kRank = false (tolerance 0 and not the last iteration): the L1 only feeds
+// the stop test, which tolerance 0 never passes, and the rank vector is only
+// read back after the last iteration -- so rank is neither read nor written
+// (16 of the 44 bytes per vertex); the contributions and the dangling mass
+// come from the new value as always.
+template <class CT, bool kRank = true>
 __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restrict__ outdeg,
                                                double* __restrict__ rank, CT* __restrict__ contrib_next,
                                                double* __restrict__ acc, double* scal, int64_t it,
@@ -558,8 +565,11 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
     const int4 od = __ldcs(reinterpret_cast<const int4*>(outdeg + v));
     const double2 a0 = __ldcs(reinterpret_cast<const double2*>(acc + v));
     const double2 a1 = __ldcs(reinterpret_cast<const double2*>(acc + v + 2));
-    const double2 r0 = __ldcs(reinterpret_cast<const double2*>(rank + v));
-    const double2 r1 = __ldcs(reinterpret_cast<const double2*>(rank + v + 2));
+    double2 r0 = make_double2(0.0, 0.0), r1 = r0;
+    if (kRank) {
+      r0 = __ldcs(reinterpret_cast<const double2*>(rank + v));
+      r1 = __ldcs(reinterpret_cast<const double2*>(rank + v + 2));
+    }
     const double nv[4] = {base + damping * a0.x, base + damping * a0.y, base + damping * a1.x,
                           base + damping * a1.y};
     const double rv[4] = {r0.x, r0.y, r1.x, r1.y};
@@ -567,14 +577,16 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
     CT c[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      l1 += fabs(nv[q] - rv[q]);
+      if (kRank) l1 += fabs(nv[q] - rv[q]);
       if (dg[q]) c[q] = (CT)(nv[q] / (double)dg[q]);
       else { c[q] = (CT)0; dm += nv[q]; }
     }
     __stcs(reinterpret_cast<double2*>(acc + v), make_double2(0.0, 0.0));
     __stcs(reinterpret_cast<double2*>(acc + v + 2), make_double2(0.0, 0.0));
-    __stcs(reinterpret_cast<double2*>(rank + v), make_double2(nv[0], nv[1]));
-    __stcs(reinterpret_cast<double2*>(rank + v + 2), make_double2(nv[2], nv[3]));
+    if (kRank) {
+      __stcs(reinterpret_cast<double2*>(rank + v), make_double2(nv[0], nv[1]));
+      __stcs(reinterpret_cast<double2*>(rank + v + 2), make_double2(nv[2], nv[3]));
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (dg[q]) contrib_next[v + q] = c[q];  // dangling entries are never gathered
@@ -590,7 +602,7 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
     }
   }
   for (int64_t v = V4 + tid; v < V; v += nth)
-    pr_vertex_one<CT>(v, outdeg, rank, contrib_next, acc, base, damping, l1, dm, peers);
+    pr_vertex_one<CT, kRank>(v, outdeg, rank, contrib_next, acc, base, damping, l1, dm, peers);
   if (peers.n) __threadfence_system();  // peer stores visible before the exchange's barrier
   l1 = block_sum(l1);
   dm = block_sum(dm);
@@ -600,12 +612,12 @@ __device__ __forceinline__ void pr_vertex_pass(int64_t V, const int32_t* __restr
   }
 }
 
-template <class CT>
+template <class CT, bool kRank = true>
 static __global__ void __launch_bounds__(256) k_pr_vertex(int64_t V, int64_t nglob, PeerSet<CT> peers,
                                                           const int32_t* outdeg, double* rank,
                                                           CT* contrib_next, double* acc, double* scal,
                                                           int64_t it, double damping) {
-  pr_vertex_pass<CT>(V, outdeg, rank, contrib_next, acc, scal, it, damping, nglob, peers);
+  pr_vertex_pass<CT, kRank>(V, outdeg, rank, contrib_next, acc, scal, it, damping, nglob, peers);
 }
 
 // Whole loop in one cooperative launch (kernel fusion on "s0").
@@ -779,15 +791,20 @@ struct PrRank {
   // next contrib slice, acc reset
   // fused all-gather: the peers' contribution buffers (same parity layout)
   std::vector<CT*> peer_c0, peer_c1;
-  void vertex(int64_t it, double damping, cudaStream_t st) {
+  // track_rank: the L1 / rank vector are needed (tolerance > 0, or the last
+  // iteration); see pr_vertex_pass
+  void vertex(int64_t it, double damping, cudaStream_t st, bool track_rank = true) {
     NvtxRange nvtx("gg.pr_block.vertex_pass");
     const int64_t lo = L->lo, n = L->vloc();
     PeerSet<CT> ps;
     ps.n = (int)peer_c0.size();
     for (int k = 0; k < ps.n; ++k) ps.p[k] = ((it & 1) ? peer_c0[k] : peer_c1[k]) + lo;
-    if (n > 0)
-      k_pr_vertex<CT><<<grid_for(n, 256, dev), 256, 0, st>>>(n, V, ps, L->outdeg.p + lo, rank + lo, nxt(it) + lo,
-                                                             acc, scal, it, damping);
+    if (n > 0 && track_rank)
+      k_pr_vertex<CT, true><<<grid_for(n, 256, dev), 256, 0, st>>>(n, V, ps, L->outdeg.p + lo, rank + lo,
+                                                                   nxt(it) + lo, acc, scal, it, damping);
+    else if (n > 0)
+      k_pr_vertex<CT, false><<<grid_for(n, 256, dev), 256, 0, st>>>(n, V, ps, L->outdeg.p + lo, rank + lo,
+                                                                    nxt(it) + lo, acc, scal, it, damping);
     GG_LAUNCH_CHECK();
     ++launches;
   }
@@ -819,7 +836,7 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
       rt.edge_begin();
       R.edges(it, st);
       rt.edge_end();
-      R.vertex(it, damping, st);
+      R.vertex(it, damping, st, tol > 0.0 || it + 1 >= max_iters);
       rt.stats.dispatch_count += 1;
       rt.stats.direction_log.push_back(s.direction);
       ++it;
@@ -910,7 +927,7 @@ int64_t pagerank_blocked_ranks(std::vector<PrRank<CT>*>& ranks, PrExchange& ex, 
     }
     rt.edge_end();
     for (size_t i = 0; i < ranks.size(); ++i) {
-      ranks[i]->vertex(it, damping, st);
+      ranks[i]->vertex(it, damping, st, tol > 0.0 || it + 1 >= max_iters);
       sc[i] = ranks[i]->scal + 2 * it + 1;
       nx[i] = ranks[i]->nxt(it);
     }
