@@ -214,7 +214,7 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   // cold windows: GG_PR_COLD_WINDOW16 sixteenths of L2 (default: the hot size)
   L->ns_cold = ns;
   if (const char* e = getenv("GG_PR_COLD_WINDOW16"))
-    L->ns_cold = std::max<int64_t>(ns, l2_bytes(g.dev) * std::max(1, atoi(e)) / 16 / ct_bytes);
+    L->ns_cold = std::max<int64_t>(1, l2_bytes(g.dev) * std::max(1, atoi(e)) / 16 / ct_bytes);
   L->K = V > ns ? 1 + (V - ns + L->ns_cold - 1) / L->ns_cold : 1;
   L->V = V;
   L->ct_bytes = ct_bytes;
