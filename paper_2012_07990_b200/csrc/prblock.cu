@@ -291,6 +291,8 @@ static PrBlockLayout* layout_for(const Graph& gc, int64_t ns, int ct_bytes, PrPa
 
 int64_t pr_block_window(const Graph& g, int ct_bytes, int64_t blocking_size) {
   if (blocking_size > 0) return blocking_size;
+  if (const char* e = getenv("GG_PR_ONE_SEGMENT"))  // A/B: every edge in the hot kernel
+    if (atoi(e) != 0) return g.V > 0 ? g.V : 1;
   // one source window in a fraction of the queried L2 (default 6/16; the
   // rest holds the streamed edges and the destination accumulators);
   // GG_PR_WINDOW16 overrides the sixteenths
@@ -376,6 +378,24 @@ __device__ __forceinline__ void pr_load_edges(const int32_t* __restrict__ src, c
 // hottest contributions (degree-renumbered ids: hot = small).
 // Gather flavours for the hot kernel (GG_PR_GATHER): 0 ld.global.nc (default),
 // 1 ld.global.cg (L2 only), 2 ld.global.nc.L1::no_allocate.
+// kLoad 3: sources past the hot window (`cold_from`) are gathered with an
+// L2 evict-first policy, so one-shot cold lines do not push the hot window
+// out of L2 (one-segment layout, GG_PR_ONE_SEGMENT)
+__device__ __forceinline__ double ld_evict_first(const double* p) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_evict_first(const float* p) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <int kLoad>
 __device__ __forceinline__ double ld_gather(const double* p) {
   if (kLoad == 1) return __ldcg(p);
@@ -399,7 +419,8 @@ __device__ __forceinline__ float ld_gather(const float* p) {
 
 template <class CT, bool kSmem, int kLoad = 0>
 __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const int32_t (&dv)[kE], const CT* contrib,
-                                               double* acc, int coherent, const CT* s_hot, int32_t nhot) {
+                                               double* acc, int coherent, const CT* s_hot, int32_t nhot,
+                                               int32_t cold_from = INT32_MAX) {
   const int lane = lane_id();
   double v[kE];
 #pragma unroll
@@ -407,6 +428,7 @@ __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const in
     if (kSmem)
       v[q] = dv[q] < 0 ? 0.0
              : su[q] < nhot ? (double)s_hot[su[q]]
+             : kLoad == 3 ? (double)(su[q] >= cold_from ? ld_evict_first(contrib + su[q]) : __ldg(contrib + su[q]))
              : (double)ld_gather<kLoad>(contrib + su[q]);
     else
       v[q] = dv[q] < 0 ? 0.0 : (double)(coherent ? ld_fresh(contrib + su[q]) : __ldg(contrib + su[q]));
@@ -459,7 +481,8 @@ __device__ __forceinline__ void pr_reduce_step(const int32_t (&su)[kE], const in
 template <class CT, bool kSmem = false, bool kPrefetch = true, int kLoad = 0>
 __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                                              int64_t e0, int64_t e1, const CT* contrib, double* acc,
-                                             int coherent, const CT* s_hot = nullptr, int32_t nhot = 0) {
+                                             int coherent, const CT* s_hot = nullptr, int32_t nhot = 0,
+                                             int32_t cold_from = INT32_MAX) {
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -472,12 +495,12 @@ __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, co
   for (; base < e1; base += stride) {
     if (!kPrefetch) {
       if (base != start + warp * 32 * kE) pr_load_edges(src, dst, base + lane * kE, e0, e1, su, dv);
-      pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot);
+      pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot, cold_from);
       continue;
     }
     int32_t nsu[kE], ndv[kE];
     pr_load_edges(src, dst, base + stride + lane * kE, e0, e1, nsu, ndv);  // dead past e1
-    pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot);
+    pr_reduce_step<CT, kSmem, kLoad>(su, dv, contrib, acc, coherent, s_hot, nhot, cold_from);
 #pragma unroll
     for (int q = 0; q < kE; ++q) {
       su[q] = nsu[q];
@@ -499,7 +522,8 @@ static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, con
 template <class CT, int kThreads, int kMinBlocks, int kLoad = 0>
 static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(const int32_t* src, const int32_t* dst,
                                                                              int64_t e0, int64_t e1, const CT* contrib,
-                                                                             double* acc, int32_t nhot) {
+                                                                             double* acc, int32_t nhot,
+                                                                             int32_t cold_from = INT32_MAX) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   CT* s_hot = reinterpret_cast<CT*>(s_raw);
   const int n4 = (int)((int64_t)nhot * sizeof(CT) / 16);
@@ -507,7 +531,7 @@ static __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pr_edges_hot(co
     reinterpret_cast<int4*>(s_raw)[i] = __ldg(reinterpret_cast<const int4*>(contrib) + i);
   for (int i = n4 * (16 / (int)sizeof(CT)) + threadIdx.x; i < nhot; i += blockDim.x) s_hot[i] = __ldg(contrib + i);
   __syncthreads();
-  pr_edges_seg<CT, true, true, kLoad>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot);
+  pr_edges_seg<CT, true, true, kLoad>(src, dst, e0, e1, contrib, acc, 0, s_hot, nhot, cold_from);
 }
 
 // Peer contribution buffers of a partitioned run with the fused all-gather:
@@ -659,6 +683,7 @@ struct HotCfg {
   int per_sm = 1;
   bool prefetch = true;
   int gather = 0;
+  int32_t cold_from = INT32_MAX;  // one-segment layout: first source past the L2 window
   unsigned grid = 0, hot_grid = 0;
 };
 
@@ -693,6 +718,16 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
   const char* pf_env = getenv("GG_PR_PREFETCH");
   h.prefetch = !(pf_env && atoi(pf_env) == 0);
   if (const char* ge = getenv("GG_PR_GATHER")) h.gather = std::max(0, std::min(2, atoi(ge)));
+  if (L->K == 1 && L->V > 1) {  // one segment: evict-first gathers past the L2-sized window
+    const int64_t w = l2_bytes(dev) * 6 / 16 / (int64_t)sizeof(CT);
+    if (w < L->V) {
+      h.cold_from = (int32_t)w;
+      h.gather = 3;
+      if (h.nhot && h.per_sm == 1)
+        GG_CUDA(cudaFuncSetAttribute((const void*)k_pr_edges_hot<CT, 1024, 1, 3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
+    }
+  }
   if (h.nhot && h.per_sm == 1 && h.gather) {
     const void* fn = h.gather == 1 ? (const void*)k_pr_edges_hot<CT, 1024, 1, 1> : (const void*)k_pr_edges_hot<CT, 1024, 1, 2>;
     GG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
@@ -769,6 +804,10 @@ struct PrRank {
       else if (sg == 0 && hc.nhot > 0 && hc.gather == 1)
         k_pr_edges_hot<CT, 1024, 1, 1><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
                                                                                        e1, c, acc, hc.nhot);
+      else if (sg == 0 && hc.nhot > 0 && hc.gather == 3)
+        k_pr_edges_hot<CT, 1024, 1, 3><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
+                                                                                       e1, c, acc, hc.nhot,
+                                                                                       hc.cold_from);
       else if (sg == 0 && hc.nhot > 0 && hc.gather == 2)
         k_pr_edges_hot<CT, 1024, 1, 2><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0,
                                                                                        e1, c, acc, hc.nhot);
