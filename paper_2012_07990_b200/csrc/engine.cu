@@ -1,3 +1,4 @@
+#include <cstdio>
 #include <map>
 #include <mutex>
 // engine.cu — edgeset.apply dispatcher, device frontiers and per-query runtime.
@@ -403,12 +404,16 @@ void* pool_alloc(size_t bytes, size_t* granted) {
     }
   }
   void* q = nullptr;
+  static const bool trace = getenv("GG_POOL_TRACE") != nullptr;
+  double t0 = trace ? now_ms() : 0.0;
   cudaError_t e = cudaMalloc(&q, c);
   if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
     cudaGetLastError();
+    if (trace) fprintf(stderr, "gg pool: out of memory at %zu bytes, trimming\n", c);
     pool_trim();
     e = cudaMalloc(&q, c);
   }
+  if (trace) fprintf(stderr, "gg pool: cudaMalloc %zu bytes %.2f ms\n", c, now_ms() - t0);
   if (e != cudaSuccess) {
     cudaGetLastError();
     fail(GG_ERR_CUDA, strf("cudaMalloc(%zu) failed: %s", c, cudaGetErrorString(e)));
