@@ -130,6 +130,10 @@ int gg_device_count(int32_t* count);
  * reused across calls instead of cudaMalloc/cudaFree each time); this
  * returns every cached block to the driver.  GG_POOL_MAX_GB caps the cache. */
 int gg_release_cached_memory(void);
+/* Pool counters since load: driver allocations, driver frees, bytes cached.
+ * When a free would push the cache past the cap, the largest cached blocks
+ * of other sizes are returned first, so per-call buffers stay cached. */
+int gg_pool_stats(int64_t* mallocs, int64_t* frees, int64_t* cached_bytes);
 int gg_device_info_get(int32_t device, gg_device_info* info);
 
 /* ---- graph (graphio.Graph.from_coo, graphio.py:58-81) ------------------------

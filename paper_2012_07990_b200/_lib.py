@@ -121,6 +121,7 @@ SIGNATURES = {
                     C.POINTER(GGStats)]),
     "gg_nccl_unique_id": (I32, [VP]),
     "gg_release_cached_memory": (I32, []),
+    "gg_pool_stats": (I32, [C.POINTER(I64)] * 3),
     "gg_comm_init": (I32, [I32, I32, I32, VP, PP]),
     "gg_comm_destroy": (I32, [VP]),
     "gg_pagerank_dist": (I32, [VP, VP, I64, F64, F64, VP, C.POINTER(GGStats)]),

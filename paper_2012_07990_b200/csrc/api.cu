@@ -142,6 +142,13 @@ int gg_release_cached_memory(void) {
   GG_API_END
 }
 
+int gg_pool_stats(int64_t* mallocs, int64_t* frees, int64_t* cached_bytes) {
+  GG_API_BEGIN
+  NEED(mallocs && frees && cached_bytes);
+  pool_counters(mallocs, frees, cached_bytes);
+  GG_API_END
+}
+
 const char* gg_version(void) { return "gg-b200 0.1.0 (sm_100a)"; }
 
 int gg_device_count(int32_t* count) {

@@ -64,6 +64,7 @@ int64_t launches_now();
 void* pool_alloc(size_t bytes, size_t* granted);
 void pool_free(void* p, size_t granted);
 void pool_trim();  // return every cached block to the driver
+void pool_counters(int64_t* mallocs, int64_t* frees, int64_t* cached);
 
 template <class T>
 struct DevBuf {

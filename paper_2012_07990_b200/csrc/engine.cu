@@ -1,6 +1,3 @@
-#include <cstdio>
-#include <map>
-#include <mutex>
 // engine.cu — edgeset.apply dispatcher, device frontiers and per-query runtime.
 //
 // Reference anchors (all in /root/reference/pkg/src/schedge/):
@@ -12,6 +9,9 @@
 //   FrontierPool                   runtime.py:124-157
 //   VertexSubset.convert/members   frontier.py:186-265
 #include "apply.cuh"
+#include <cstdio>
+#include <map>
+#include <mutex>
 #include <cub/device/device_select.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -349,6 +349,7 @@ struct DevicePool {
   std::mutex mu;
   std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;
   size_t cached = 0;
+  int64_t mallocs = 0, frees = 0;
 };
 DevicePool& pool() {
   static DevicePool* p = new DevicePool;  // never destroyed: frees at exit are unordered
@@ -363,13 +364,12 @@ size_t size_class(size_t bytes) {
   const size_t g = 2u << 20;
   return (bytes + g - 1) / g * g;
 }
-// cache at most this many bytes (beyond it, frees go to the driver)
+// cache at most this many bytes (beyond it, frees go to the driver); read on
+// every free so a process can lower it between queries
 size_t pool_limit() {
-  static size_t lim = [] {
-    const char* e = getenv("GG_POOL_MAX_GB");
-    return (size_t)(e ? atof(e) : 48.0) * (size_t(1) << 30);
-  }();
-  return lim;
+  const char* e = getenv("GG_POOL_MAX_GB");
+  const double gb = e ? atof(e) : 48.0;
+  return gb > 0 ? (size_t)(gb * (double)(size_t(1) << 30)) : 0;
 }
 }  // namespace
 
@@ -381,10 +381,19 @@ void pool_trim() {
   for (auto& kv : P.free_blocks) {
     cudaSetDevice(kv.first.first);
     for (void* q : kv.second) cudaFree(q);
+    P.frees += (int64_t)kv.second.size();
   }
   cudaSetDevice(cur);
   P.free_blocks.clear();
   P.cached = 0;
+}
+
+void pool_counters(int64_t* mallocs, int64_t* frees, int64_t* cached) {
+  DevicePool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  *mallocs = P.mallocs;
+  *frees = P.frees;
+  *cached = (int64_t)P.cached;
 }
 
 void* pool_alloc(size_t bytes, size_t* granted) {
@@ -414,6 +423,10 @@ void* pool_alloc(size_t bytes, size_t* granted) {
     e = cudaMalloc(&q, c);
   }
   if (trace) fprintf(stderr, "gg pool: cudaMalloc %zu bytes %.2f ms\n", c, now_ms() - t0);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.mallocs += 1;
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     fail(GG_ERR_CUDA, strf("cudaMalloc(%zu) failed: %s", c, cudaGetErrorString(e)));
@@ -429,15 +442,41 @@ void pool_free(void* q, size_t granted) {
   if (cudaPointerGetAttributes(&at, q) == cudaSuccess) dev = at.device;
   else if (cudaGetDevice(&dev) != cudaSuccess) return;
   DevicePool& P = pool();
+  std::vector<std::pair<int, void*>> evict;
   {
     std::lock_guard<std::mutex> lk(P.mu);
-    if (P.cached + granted <= pool_limit()) {
-      P.free_blocks[{dev, granted}].push_back(q);
-      P.cached += granted;
-      return;
+    if (granted > pool_limit()) {
+      evict.push_back({dev, q});
+    } else {
+      // Make room by returning the largest cached blocks of OTHER size
+      // classes: one-off temporaries (graph build sort buffers) go, while a
+      // block that is freed and re-requested every call stays cached
+      // (otherwise every call pays a synchronising cudaFree + cudaMalloc).
+      for (auto it = P.free_blocks.rbegin(); P.cached + granted > pool_limit() && it != P.free_blocks.rend(); ++it) {
+        if (it->first == std::make_pair(dev, granted)) continue;
+        while (!it->second.empty() && P.cached + granted > pool_limit()) {
+          evict.push_back({it->first.first, it->second.back()});
+          it->second.pop_back();
+          P.cached -= it->first.second;
+        }
+      }
+      if (P.cached + granted <= pool_limit()) {
+        P.free_blocks[{dev, granted}].push_back(q);
+        P.cached += granted;
+      } else {
+        evict.push_back({dev, q});
+      }
     }
+    P.frees += (int64_t)evict.size();
   }
-  cudaFree(q);
+  if (evict.empty()) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& e : evict) {
+    cudaSetDevice(e.first);
+    cudaFree(e.second);
+  }
+  cudaSetDevice(cur);
 }
 
 void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n) {

@@ -181,3 +181,16 @@ class EdgeContext:
     def __init__(self, *a, **k):
         raise EngineError("EdgeContext callbacks cannot run on the device; use a named "
                           "device UDF from paper_2012_07990_b200.udfs")
+
+
+def pool_stats():
+    """Device caching-pool counters: {"mallocs", "frees", "cached_bytes"}
+    (driver allocations and frees since the library loaded)."""
+    m, f, c = C.c_int64(), C.c_int64(), C.c_int64()
+    _lib.call("gg_pool_stats", C.byref(m), C.byref(f), C.byref(c))
+    return {"mallocs": m.value, "frees": f.value, "cached_bytes": c.value}
+
+
+def release_cached_memory():
+    """Return every cached device block to the driver."""
+    _lib.call("gg_release_cached_memory")

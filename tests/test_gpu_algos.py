@@ -364,3 +364,20 @@ def test_bfs_more_vertices_than_grid_threads(gg, sch):
         r = gg.bfs(g, src, prog)
         assert np.array_equal(np.asarray(gg.bfs_levels(r.array)),
                               oracle.bfs_levels(V, off, nbr, src, parallel=True))
+
+
+def test_pool_keeps_per_call_buffers_under_cap(gg, monkeypatch):
+    """With the cache cap below what the graph build left cached, a repeat
+    query must still find its buffers in the pool (one-off build temporaries
+    are evicted instead): no driver allocation on the second identical call."""
+    from paper_2012_07990_b200.runtime import pool_stats
+    monkeypatch.setenv("GG_POOL_MAX_GB", "0.125")
+    g = gg.generate_rmat(17, 16, seed=3, symmetrize=True)
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance="TWC"))
+    first = gg.bc(g, [0, 7], prog).array
+    before = pool_stats()
+    again = gg.bc(g, [0, 7], prog).array
+    after = pool_stats()
+    assert after["mallocs"] == before["mallocs"], (before, after)
+    assert after["cached_bytes"] <= int(0.125 * 2**30)
+    close_bc(again, first)  # f64 atomic order differs between calls
