@@ -128,7 +128,8 @@ const char* gg_version(void);
 int gg_device_count(int32_t* count);
 /* Device buffers come from a per-device caching pool (per-query buffers are
  * reused across calls instead of cudaMalloc/cudaFree each time); this
- * returns every cached block to the driver.  GG_POOL_MAX_GB caps the cache. */
+ * returns every cached block to the driver.  GG_POOL_MAX_GB caps the cache
+ * (default: 60% of the device's memory). */
 int gg_release_cached_memory(void);
 /* Pool counters since load: driver allocations, driver frees, bytes cached.
  * When a free would push the cache past the cap, the largest cached blocks

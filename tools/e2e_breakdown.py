@@ -41,5 +41,7 @@ for step in range(3):
     t3 = time.perf_counter()
     ge.close()
     t4 = time.perf_counter()
+    ps = gg.runtime.pool_stats()
+    print("pool: %d mallocs %d frees %.1f GB cached" % (ps["mallocs"], ps["frees"], ps["cached_bytes"] / 2**30))
     print("step %d: create+H2D %.3f s  layout %.3f s  pagerank(20 it + D2H) %.3f s (kernel %.3f ms)  close %.3f s  total %.3f s"
           % (step, t1 - t0, t2 - t1, t3 - t2, r.stats.kernel_ms, t4 - t3, t4 - t0))
