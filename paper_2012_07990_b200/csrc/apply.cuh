@@ -12,7 +12,7 @@ void clear_marks(Runtime* rt, Frontier* out, const OutBuilder& ob);
 Frontier* converted_view(Runtime* rt, Frontier* in, int repr);
 void twc_queues(Runtime* rt, TwcQueues* q);
 // ETWC huge-range queue (capacity E / kEtwcHuge + 1), count zeroed on the stream
-void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n);
+void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small_frontier = 0);
 OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out);
 void dense_size_on_device(Frontier* f, cudaStream_t s);
 
@@ -36,7 +36,13 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
       k_push_cm<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
       break;
     case GG_LB_ETWC: {
-      etwc_huge(rt, &a.huge, &a.huge_n);
+      // A frontier that fills fewer than two CTAs per SM would leave every
+      // CTA-stage range (>= cta arcs) on a handful of CTAs (a 744-vertex
+      // BFS level of RMAT-24 with hub neighbours: 3.1 ms on 3 CTAs): all of
+      // them go to the chunk-balanced grid pass instead.
+      const bool small = work < (int64_t)sm_count(dev) * 2 * 256;
+      etwc_huge(rt, &a.huge, &a.huge_n, small ? work : 0);
+      if (small && a.huge) a.huge_min = cta;
       k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
       if (a.huge) {
         k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);

@@ -5,6 +5,8 @@
 // the bound schedule or hybrid switch, input frontier recycled (reuse=True),
 // loop until the output frontier is empty (engine.fused_loop).
 #include "engine.cuh"
+#include <cstdio>
+#include <cstdlib>
 
 namespace gg {
 
@@ -30,12 +32,26 @@ void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, R
   }
   std::unique_ptr<Frontier> frontier = rt.new_frontier(&src32, 1);
   gg_udf_state ust{parent.p, nullptr, 0};
+  static const bool trace = getenv("GG_ROUND_TRACE") != nullptr;
+  std::vector<int64_t> sizes;
   while (frontier_size(&rt, frontier.get()) > 0) {
+    if (trace) sizes.push_back(frontier_size(&rt, frontier.get()));
     rt.edge_begin();
     std::unique_ptr<Frontier> out = edgeset_apply(&rt, UDF_BFS, ust, true, &frontier, b, true, true);
     rt.edge_end();
     frontier = std::move(out);
     rt.stats.rounds += 1;
+  }
+  if (trace) {  // per-round input size, direction and edge-phase time
+    const size_t base = rt.edge_events.size() - sizes.size();
+    for (size_t i = 0; i < sizes.size(); ++i) {
+      auto& ev = rt.edge_events[base + i];
+      GG_CUDA(cudaEventSynchronize(ev.second));
+      float ms = 0;
+      GG_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+      fprintf(stderr, "bfs round %zu: |in| %lld %s %.3f ms\n", i, (long long)sizes[i],
+              rt.stats.direction_log[rt.stats.direction_log.size() - sizes.size() + i] == GG_PUSH ? "push" : "pull", ms);
+    }
   }
   GG_CUDA(cudaMemcpyAsync(parents_out, parent.p, g.V * sizeof(int32_t), cudaMemcpyDefault, st));
   GG_CUDA(cudaStreamSynchronize(st));

@@ -494,14 +494,16 @@ void pool_free(void* q, size_t granted) {
   cudaSetDevice(cur);
 }
 
-void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n) {
+void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small_frontier) {
   rt->g->ensure_out();
-  if (rt->g->max_out_degree < kEtwcHuge) {  // no hub: no grid pass (no extra barriers)
+  // no hub and a frontier that fills the grid: no grid pass (no extra barriers)
+  if (rt->g->max_out_degree < kEtwcHuge && (small_frontier == 0 || rt->g->max_out_degree < rt->cfg.cta_size)) {
     *q = nullptr;
     *n = nullptr;
     return;
   }
-  const int64_t cap = rt->g->E / kEtwcHuge + 1;
+  // one entry per active vertex at most; per kEtwcHuge arcs for the hub pass
+  const int64_t cap = std::max(rt->g->E / kEtwcHuge, small_frontier) + 1;
   if (rt->etwc_q.n < (size_t)cap) rt->etwc_q.alloc(cap);
   if (!rt->etwc_n.p) rt->etwc_n.alloc(1);
   GG_CUDA(cudaMemsetAsync(rt->etwc_n.p, 0, sizeof(unsigned long long), rt->stream));

@@ -186,6 +186,7 @@ struct PushArgs {
   // queue and are processed by the whole grid afterwards (null: in-CTA)
   EtwcEntry* huge = nullptr;
   unsigned long long* huge_n = nullptr;
+  int64_t huge_min = 16384;  // kEtwcHuge; the CTA size for small frontiers (run_push)
 };
 
 template <class Op>
@@ -503,15 +504,65 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
   for (; e < hi; e += stride) push_edge(a, u, e);
 }
 
-// grid-wide pass over the huge CTA-stage ranges queued by b_push_etwc
+// Grid-wide pass over the CTA-stage ranges queued by b_push_etwc.  The
+// ranges are cut into chunks of kHugeChunk arcs, numbered in queue order, and
+// chunk j goes to CTA j mod gridDim (each CTA walks its chunks with all its
+// threads), so the work is balanced over the whole grid however the arcs are
+// spread over the ranges.  The queue is read 256 entries at a time: a block
+// scan of the per-entry chunk counts, then a binary search per chunk.
+constexpr int64_t kHugeChunk = 2048;
 template <class Op>
 __device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
+  __shared__ EtwcEntry s_e[256];
+  __shared__ int64_t s_end[256];  // inclusive prefix of chunk counts in the batch
+  __shared__ int64_t s_w[8];
   const int64_t n = (int64_t)*((volatile unsigned long long*)a.huge_n);
-  const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = 0; k < n; ++k) {
-    const EtwcEntry c = a.huge[k];
-    push_range_strided(a, c.u, c.lo, c.hi(), first, stride);
+  const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t G = gridDim.x;
+  int64_t gchunk = 0;  // chunks of the batches before this one
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    int64_t x = 0;
+    if (i < n) {
+      const EtwcEntry c = a.huge[i];
+      s_e[threadIdx.x] = c;
+      x = (c.len + kHugeChunk - 1) / kHugeChunk;
+    }
+#pragma unroll
+    for (int o = 1; o < kWarp; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == kWarp - 1) s_w[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t t = lane < nw ? s_w[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      if (lane < nw) s_w[lane] = t;
+    }
+    __syncthreads();
+    if (wid > 0) x += s_w[wid - 1];
+    s_end[threadIdx.x] = x;
+    __syncthreads();
+    const int64_t total = s_end[blockDim.x - 1];
+    const int last = (int)min((int64_t)blockDim.x, n - base) - 1;
+    for (int64_t j = ((int64_t)blockIdx.x - gchunk % G + G) % G; j < total; j += G) {
+      int lo = 0, hi = last;  // first entry whose prefix end exceeds j
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_end[mid] > j) hi = mid; else lo = mid + 1;
+      }
+      const EtwcEntry c = s_e[lo];
+      const int64_t first = s_end[lo] - (c.len + kHugeChunk - 1) / kHugeChunk;
+      const int64_t clo = c.lo + (j - first) * kHugeChunk;
+      push_range_strided(a, c.u, clo, min(clo + kHugeChunk, c.hi()), threadIdx.x, blockDim.x);
+    }
+    gchunk += total;
+    __syncthreads();
   }
 }
 template <class Op>
@@ -545,7 +596,7 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
     int64_t e0 = size - e2 - e1;
     EtwcEntry c2{start, (int32_t)e2, u}, c1{start + e2, (int32_t)e1, u},
         c0{start + e2 + e1, (int32_t)e0, u};
-    if (a.huge && e2 >= kEtwcHuge) {  // whole-grid pass after this kernel / phase
+    if (a.huge && e2 >= a.huge_min) {  // whole-grid pass after this kernel / phase
       a.huge[atomicAdd(a.huge_n, 1ULL)] = c2;
       e2 = 0;
     }
