@@ -63,7 +63,7 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
       a.scanned = rt->scanned.p;
       k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
       k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
-      k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      k_twc_cta<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a, q.q[2], q.cnt + 2);
       count_launch(3);
       break;
     }

@@ -20,14 +20,27 @@ void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, R
   check_binding(b);
   DeviceGuard guard(g.dev);
   cudaStream_t st = rt.stream;
-  DevBuf<int32_t> parent(g.V);
+  // a device result buffer on this device is the working array (no copy)
+  cudaPointerAttributes at{};
+  bool direct = false;
+  if (cudaPointerGetAttributes(&at, parents_out) == cudaSuccess)
+    direct = at.type == cudaMemoryTypeDevice && at.device == g.dev;
+  else
+    cudaGetLastError();
+  DevBuf<int32_t> scratch;
+  if (!direct) scratch.alloc(g.V);
+  struct { int32_t* p; } parent{direct ? parents_out : scratch.p};
+  auto finish = [&] {
+    if (!direct)
+      GG_CUDA(cudaMemcpyAsync(parents_out, parent.p, g.V * sizeof(int32_t), cudaMemcpyDefault, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+  };
   GG_CUDA(cudaMemsetAsync(parent.p, 0xff, g.V * sizeof(int32_t), st));
   int32_t src32 = (int32_t)source;
   GG_CUDA(cudaMemcpyAsync(parent.p + source, &src32, 4, cudaMemcpyHostToDevice, st));
   if (fusion) {
     bfs_fused(rt, b, parent.p, src32);
-    GG_CUDA(cudaMemcpyAsync(parents_out, parent.p, g.V * sizeof(int32_t), cudaMemcpyDefault, st));
-    GG_CUDA(cudaStreamSynchronize(st));
+    finish();
     return;
   }
   std::unique_ptr<Frontier> frontier = rt.new_frontier(&src32, 1);
@@ -53,8 +66,7 @@ void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, R
               rt.stats.direction_log[rt.stats.direction_log.size() - sizes.size() + i] == GG_PUSH ? "push" : "pull", ms);
     }
   }
-  GG_CUDA(cudaMemcpyAsync(parents_out, parent.p, g.V * sizeof(int32_t), cudaMemcpyDefault, st));
-  GG_CUDA(cudaStreamSynchronize(st));
+  finish();
 }
 
 }  // namespace gg

@@ -295,6 +295,21 @@ __global__ void k_check_ids(const int32_t* ids, int64_t n, int64_t V, int* bad) 
 std::unique_ptr<Frontier> Runtime::new_frontier(const int32_t* ids, int64_t n) {
   auto f = acquire(GG_SPARSE);
   if (n > (int64_t)f->ids.n) fail(GG_ERR_ENGINE, "frontier larger than its capacity");
+  cudaPointerAttributes at{};
+  bool host = true;
+  if (cudaPointerGetAttributes(&at, ids) == cudaSuccess) host = at.type == cudaMemoryTypeUnregistered || at.type == cudaMemoryTypeHost;
+  else cudaGetLastError();
+  if (host && n <= 4096) {
+    // small host list (a BFS / BC source): check on the host, no round trip;
+    // pageable copies are staged before cudaMemcpyAsync returns
+    for (int64_t i = 0; i < n; ++i)
+      if (ids[i] < 0 || ids[i] >= g->V) fail(GG_ERR_ENGINE, "vertex id out of range");
+    if (n) GG_CUDA(cudaMemcpyAsync(f->ids.p, ids, n * 4, cudaMemcpyHostToDevice, stream));
+    unsigned long long hn = (unsigned long long)n;
+    GG_CUDA(cudaMemcpyAsync(f->count.p, &hn, 8, cudaMemcpyHostToDevice, stream));
+    f->size_cache = n;
+    return f;
+  }
   if (n) {
     GG_CUDA(cudaMemcpyAsync(f->ids.p, ids, n * 4, cudaMemcpyDefault, stream));
     DevBuf<int> bad(1);

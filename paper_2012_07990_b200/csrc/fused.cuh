@@ -23,6 +23,7 @@ struct FusedScratch {
   CooView blocked;
   EtwcEntry* etwc_q;             // ETWC huge CTA-stage ranges (grid pass)
   unsigned long long* etwc_n;    // kept 0 between phases
+  int64_t etwc_small;            // active lists shorter than this send every CTA-stage range to the grid pass
 };
 
 // Grid-wide exclusive prefix of active out-degrees (STRICT push in a fused
@@ -103,6 +104,7 @@ __device__ __forceinline__ void fused_edge_phase(const gg_schedule& s, const Csr
       case GG_LB_ETWC:
         a.huge = sc.etwc_q;
         a.huge_n = sc.etwc_n;
+        if (a.huge && active_count(in, out_csr.V) < sc.etwc_small) a.huge_min = cta;  // as run_push
         b_push_etwc<Op>(a, cta);
         if (a.huge) {
           grid.sync();
@@ -161,7 +163,10 @@ struct FusedHost {
     for (int k = 0; k < nsched; ++k) {
       const gg_schedule& s = *scheds[k];
       if (s.load_balance == GG_LB_TWC) twc_queues(&rt, &sc.twc);
-      if (s.load_balance == GG_LB_ETWC && s.direction == GG_PUSH) etwc_huge(&rt, &sc.etwc_q, &sc.etwc_n);
+      if (s.load_balance == GG_LB_ETWC && s.direction == GG_PUSH) {
+        sc.etwc_small = (int64_t)sm_count(rt.dev) * 2 * 256;
+        etwc_huge(&rt, &sc.etwc_q, &sc.etwc_n, sc.etwc_small);
+      }
       if (s.load_balance == GG_LB_STRICT && s.direction == GG_PUSH) {
         prefix.alloc(g.V + 2);
         block_sums.alloc(coop_blocks + 1);

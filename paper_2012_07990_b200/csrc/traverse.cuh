@@ -428,21 +428,6 @@ __global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t*
   b_twc_warp<Op>(a, qu, cnt);
 }
 
-template <class Op>
-__device__ __forceinline__ void b_twc_cta(PushArgs<Op> a, const int32_t* qu,
-                                                 const unsigned long long* cnt) {
-  const int64_t n = (int64_t)*cnt;
-  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-    int32_t u = qu[i];
-    int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) push_edge(a, u, e);
-  }
-}
-template <class Op>
-__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
-                                                 const unsigned long long* cnt) {
-  b_twc_cta<Op>(a, qu, cnt);
-}
 
 // ETWC (engine.py:51-85, 186-193; paper Alg. 3).  Each CTA takes blockDim
 // contiguous active vertices; every vertex's range is split into a
@@ -511,12 +496,11 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
 // spread over the ranges.  The queue is read 256 entries at a time: a block
 // scan of the per-entry chunk counts, then a binary search per chunk.
 constexpr int64_t kHugeChunk = 2048;
-template <class Op>
-__device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
+template <class Op, class Src>
+__device__ __forceinline__ void push_ranges_chunked(const PushArgs<Op>& a, int64_t n, Src src) {
   __shared__ EtwcEntry s_e[256];
   __shared__ int64_t s_end[256];  // inclusive prefix of chunk counts in the batch
   __shared__ int64_t s_w[8];
-  const int64_t n = (int64_t)*((volatile unsigned long long*)a.huge_n);
   const int lane = lane_id(), wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t G = gridDim.x;
   int64_t gchunk = 0;  // chunks of the batches before this one
@@ -524,7 +508,7 @@ __device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
     const int64_t i = base + threadIdx.x;
     int64_t x = 0;
     if (i < n) {
-      const EtwcEntry c = a.huge[i];
+      const EtwcEntry c = src(i);
       s_e[threadIdx.x] = c;
       x = (c.len + kHugeChunk - 1) / kHugeChunk;
     }
@@ -566,8 +550,32 @@ __device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
   }
 }
 template <class Op>
+__device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
+  const int64_t n = (int64_t)*((volatile unsigned long long*)a.huge_n);
+  push_ranges_chunked(a, n, [&](int64_t i) { return a.huge[i]; });
+}
+template <class Op>
 __global__ void __launch_bounds__(256) k_push_huge(PushArgs<Op> a) {
   b_push_huge<Op>(a);
+}
+
+// TWC's CTA bin: the binned vertices' whole ranges, cut into chunks dealt
+// over the grid like the ETWC grid pass (one CTA per hub serialised the
+// launch on Kronecker hubs: 19 ms per BC forward round).
+template <class Op>
+__device__ __forceinline__ void b_twc_cta(PushArgs<Op> a, const int32_t* qu,
+                                                 const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*((volatile unsigned long long*)cnt);
+  push_ranges_chunked(a, n, [&](int64_t i) {
+    const int32_t u = qu[i];
+    const int64_t lo = __ldg(a.g.off + u);
+    return EtwcEntry{lo, (int32_t)(__ldg(a.g.off + u + 1) - lo), u};
+  });
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
+                                                 const unsigned long long* cnt) {
+  b_twc_cta<Op>(a, qu, cnt);
 }
 
 template <class Op>
