@@ -36,11 +36,12 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
       k_push_cm<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a);
       break;
     case GG_LB_ETWC: {
-      // A frontier that fills fewer than two CTAs per SM would leave every
-      // CTA-stage range (>= cta arcs) on a handful of CTAs (a 744-vertex
-      // BFS level of RMAT-24 with hub neighbours: 3.1 ms on 3 CTAs): all of
-      // them go to the chunk-balanced grid pass instead.
-      const bool small = work < (int64_t)sm_count(dev) * 2 * 256;
+      // A frontier that fills only a few CTAs (one per 256 vertices) would
+      // leave every CTA-stage range (>= cta arcs) on a handful of SMs (a
+      // 744-vertex BFS level of RMAT-24 with hub neighbours: 3.1 ms on 3
+      // CTAs): all of them go to the chunk-balanced grid pass instead.  The
+      // bound keeps the pass's per-CTA walk of the queue short.
+      const bool small = work < kEtwcSmallPerSm * sm_count(dev);
       etwc_huge(rt, &a.huge, &a.huge_n, small ? work : 0);
       if (small && a.huge) a.huge_min = cta;
       k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
@@ -59,12 +60,17 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
     case GG_LB_TWC: {
       TwcQueues q;
       twc_queues(rt, &q);
+      etwc_huge(rt, &a.huge, &a.huge_n);  // hubs skip the bins (b_twc_bin)
       k_twc_bin<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q, cta);
       a.scanned = rt->scanned.p;
       k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
       k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
-      k_twc_cta<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
       count_launch(3);
+      if (a.huge) {
+        k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+        count_launch();
+      }
       break;
     }
     default:

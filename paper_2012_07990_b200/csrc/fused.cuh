@@ -164,7 +164,7 @@ struct FusedHost {
       const gg_schedule& s = *scheds[k];
       if (s.load_balance == GG_LB_TWC) twc_queues(&rt, &sc.twc);
       if (s.load_balance == GG_LB_ETWC && s.direction == GG_PUSH) {
-        sc.etwc_small = (int64_t)sm_count(rt.dev) * 2 * 256;
+        sc.etwc_small = kEtwcSmallPerSm * sm_count(rt.dev);
         etwc_huge(&rt, &sc.etwc_q, &sc.etwc_n, sc.etwc_small);
       }
       if (s.load_balance == GG_LB_STRICT && s.direction == GG_PUSH) {

@@ -174,6 +174,13 @@ __device__ __forceinline__ int upper_idx(F key, int n, int64_t x) {
 // udf with atomic helpers.
 // ===========================================================================
 struct EtwcEntry;
+// a queued arc range [lo, lo + len) of source u (ETWC / hub grid pass)
+struct EtwcEntry {
+  int64_t lo;
+  int32_t len;
+  int32_t u;
+  __device__ __forceinline__ int64_t hi() const { return lo + len; }
+};
 template <class Op>
 struct PushArgs {
   CsrView g;
@@ -376,8 +383,13 @@ __device__ __forceinline__ void b_twc_bin(PushArgs<Op> a, TwcQueues q, int cta) 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t u = active_at(a.in, i);
-    int64_t deg = __ldg(a.g.off + u + 1) - __ldg(a.g.off + u);
+    const int64_t lo = __ldg(a.g.off + u);
+    int64_t deg = __ldg(a.g.off + u + 1) - lo;
     sc += deg;
+    if (a.huge && deg >= a.huge_min) {  // hub: the chunked grid pass (run_push)
+      a.huge[atomicAdd(a.huge_n, 1ULL)] = EtwcEntry{lo, (int32_t)deg, u};
+      continue;
+    }
     int b = deg > cta ? 2 : (deg > kWarp ? 1 : 0);
     cg::coalesced_group g = cg::coalesced_threads();
     cg::coalesced_group gb = cg::labeled_partition(g, b);
@@ -428,22 +440,39 @@ __global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t*
   b_twc_warp<Op>(a, qu, cnt);
 }
 
+// (Dealing the whole CTA bin over the grid in chunks, like the ETWC grid
+// pass, measured slower for CC on Kronecker-25 -- 66 vs 85 GTEPS: the bin
+// holds ~10^6 ranges and every CTA walks the whole bin to number the chunks;
+// only hubs of >= kEtwcHuge arcs take that pass, queued by b_twc_bin.)
+template <class Op>
+__device__ __forceinline__ void b_twc_cta(PushArgs<Op> a, const int32_t* qu,
+                                                 const unsigned long long* cnt) {
+  const int64_t n = (int64_t)*cnt;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    int32_t u = qu[i];
+    int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
+    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) push_edge(a, u, e);
+  }
+}
+template <class Op>
+__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
+                                                 const unsigned long long* cnt) {
+  b_twc_cta<Op>(a, qu, cnt);
+}
+
 
 // ETWC (engine.py:51-85, 186-193; paper Alg. 3).  Each CTA takes blockDim
 // contiguous active vertices; every vertex's range is split into a
 // CTA-multiple (Q2), warp-multiple (Q1) and remainder (Q0) chunk, queued in
 // shared memory (warp ballot + CTA prefix for slots), then the stages run in
 // order 0, 1, 2 with thread / warp / CTA cooperative processing.
-struct EtwcEntry {
-  int64_t lo;
-  int32_t len;
-  int32_t u;
-  __device__ __forceinline__ int64_t hi() const { return lo + len; }
-};
 // A single CTA walking a hub's whole CTA-stage range serialises on the hub
 // (RMAT/Kronecker hubs have 10^5-10^6 arcs, several can land in one CTA's
 // slice of the active list): such ranges are handed to the whole grid.
 constexpr int64_t kEtwcHuge = 16384;
+// active lists shorter than kEtwcSmallPerSm x SMs (< 1 CTA per 4 SMs) send
+// every CTA-stage range to the grid pass (run_push, fused loops)
+constexpr int64_t kEtwcSmallPerSm = 64;
 
 // Ops whose push is "accumulate into the SOURCE" (BC backward: delta[u] +=
 // f(v)) declare kPushReduce and provide push_val / push_commit: a range walk
@@ -557,25 +586,6 @@ __device__ __forceinline__ void b_push_huge(PushArgs<Op> a) {
 template <class Op>
 __global__ void __launch_bounds__(256) k_push_huge(PushArgs<Op> a) {
   b_push_huge<Op>(a);
-}
-
-// TWC's CTA bin: the binned vertices' whole ranges, cut into chunks dealt
-// over the grid like the ETWC grid pass (one CTA per hub serialised the
-// launch on Kronecker hubs: 19 ms per BC forward round).
-template <class Op>
-__device__ __forceinline__ void b_twc_cta(PushArgs<Op> a, const int32_t* qu,
-                                                 const unsigned long long* cnt) {
-  const int64_t n = (int64_t)*((volatile unsigned long long*)cnt);
-  push_ranges_chunked(a, n, [&](int64_t i) {
-    const int32_t u = qu[i];
-    const int64_t lo = __ldg(a.g.off + u);
-    return EtwcEntry{lo, (int32_t)(__ldg(a.g.off + u + 1) - lo), u};
-  });
-}
-template <class Op>
-__global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
-                                                 const unsigned long long* cnt) {
-  b_twc_cta<Op>(a, qu, cnt);
 }
 
 template <class Op>

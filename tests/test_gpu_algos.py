@@ -273,12 +273,16 @@ def hub_graph(gg):
     return g, off, nbr
 
 
+@pytest.mark.parametrize("lb", ["ETWC", "TWC"])
 @pytest.mark.parametrize("fusion", [False, True])
-def test_etwc_hub_pass_bfs_cc(gg, hub_graph, fusion):
+def test_etwc_hub_pass_bfs_cc(gg, hub_graph, fusion, lb):
+    """ETWC hub ranges go through the chunk-balanced grid pass (ranges of
+    >= 16384 arcs, or every CTA-stage range for a small frontier); TWC's CTA
+    bin walks them one CTA per vertex."""
     g, off, nbr = hub_graph
     V = g.num_vertices
     assert int(np.max(np.diff(off))) >= 16384
-    prog = program_with(gg.Schedule(direction="PUSH", load_balance="ETWC"), fusion=fusion)
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance=lb), fusion=fusion)
     for src in (0, 7, 150):
         r = gg.bfs(g, src, prog)
         assert gg.bfs_levels(r.values) == oracle.bfs_levels(V, off, nbr, src).tolist()
@@ -288,9 +292,10 @@ def test_etwc_hub_pass_bfs_cc(gg, hub_graph, fusion):
     assert np.array_equal(gg.cc_soman(g, prog).array, want)
 
 
-def test_etwc_hub_pass_bc(gg, hub_graph):
+@pytest.mark.parametrize("lb", ["ETWC", "TWC"])
+def test_etwc_hub_pass_bc(gg, hub_graph, lb):
     g, off, nbr = hub_graph
-    prog = program_with(gg.Schedule(direction="PUSH", load_balance="ETWC"))
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance=lb))
     srcs = [0, 150, 7]
     close_bc(gg.bc(g, srcs, prog).values, oracle.bc(g.num_vertices, off, nbr, srcs))
 
@@ -381,3 +386,31 @@ def test_pool_keeps_per_call_buffers_under_cap(gg, monkeypatch):
     assert after["mallocs"] == before["mallocs"], (before, after)
     assert after["cached_bytes"] <= int(0.125 * 2**30)
     close_bc(again, first)  # f64 atomic order differs between calls
+
+
+@pytest.mark.parametrize("lb", ["ETWC", "TWC"])
+def test_chunked_pass_many_ranges(gg, lb):
+    """Over 256 queued CTA-stage ranges of mixed lengths (several block-scan
+    batches, chunks straddling batch boundaries): BFS levels, arcs scanned and
+    CC labels exact."""
+    rng = np.random.default_rng(17)
+    V = 40000
+    mids = np.arange(1, 701)
+    degs = rng.integers(257, 3000, size=mids.size)
+    src = [np.zeros(mids.size, np.int64)]
+    dst = [mids.astype(np.int64)]
+    for m, k in zip(mids, degs):
+        src.append(np.full(k, m, np.int64))
+        dst.append(rng.integers(1000, V, size=k))
+    s = np.concatenate(src); d = np.concatenate(dst)
+    keep = s != d
+    from paper_2012_07990_b200.graphio import symmetrize_coo
+    s2, d2, _, _ = symmetrize_coo(s[keep], d[keep])
+    g = gg.Graph.from_coo(V, s2, d2, symmetric=True)
+    off, nbr, _ = oracle.csr(V, g.coo_src, g.coo_dst)
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance=lb))
+    r = gg.bfs(g, 0, prog)
+    assert gg.bfs_levels(r.values) == oracle.bfs_levels(V, off, nbr, 0).tolist()
+    assert r.stats.edges_traversed == int(sum(np.diff(off)[np.asarray(r.values) >= 0]))
+    want, _ = oracle.cc(V, g.coo_src, g.coo_dst)
+    assert np.array_equal(gg.cc_soman(g, prog).array, want)
