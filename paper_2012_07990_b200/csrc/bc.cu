@@ -51,12 +51,7 @@ static int64_t snapshot(Runtime& rt, Frontier* f, int32_t* order, int64_t pos, D
     GG_CUDA(cudaMemcpyAsync(order + pos, f->ids.p, cnt * 4, cudaMemcpyDeviceToDevice, st));
     return cnt;
   }
-  DenseMember pred{f->repr == GG_BITMAP ? f->bits.p : nullptr, f->repr == GG_BOOLMAP ? f->bools.p : nullptr};
-  cub::CountingInputIterator<int32_t> it(0);
-  size_t temp = 0;
-  GG_CUDA(cub::DeviceSelect::If(nullptr, temp, it, order + pos, n.p, rt.g->V, pred, st));
-  GG_CUDA(cub::DeviceSelect::If(rt.cub_tmp.get(temp), temp, it, order + pos, n.p, rt.g->V, pred, st));
-  count_launch();
+  dense_to_sparse(f, order + pos, n.p, st);
   return cnt;
 }
 

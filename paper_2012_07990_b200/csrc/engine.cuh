@@ -93,6 +93,8 @@ std::unique_ptr<Frontier> frontier_alloc(int dev, int64_t universe, int repr, in
 void frontier_clear(Frontier* f, cudaStream_t s);
 // convert into `dst` (allocated by caller with the target repr)
 void frontier_convert_into(Runtime* rt, Frontier* src, Frontier* dst);
+// members of a BITMAP / BOOLMAP frontier, ascending, into out[0..*count)
+void dense_to_sparse(const Frontier* src, int32_t* out, unsigned long long* count, cudaStream_t s);
 
 // Host-side schedule validation (sched.validate, sched.py:123-142).
 void check_schedule(const gg_schedule& s);

@@ -167,3 +167,25 @@ def test_errors(gg, golden_small):
     with pytest.raises(gg.ScheduleError, match="unresolved"):
         gg.hybrid_apply(g, None, gg.udfs.EnqueueDst(), gg.udfs.EnqueueDst(),
                         gg.HybridSchedule(threshold="argv[3]"))
+
+
+@pytest.mark.parametrize("V", [1, 31, 33, 1000, 32768, 32769, 100003])
+@pytest.mark.parametrize("target", ["BITMAP", "BOOLMAP"])
+def test_dense_sparse_round_trip(gg, V, target):
+    """SPARSE -> dense -> SPARSE gives the members ascending and deduplicated
+    (frontier.py:186-201, 242-265) at ragged universes: partial last mask,
+    several 32768-vertex blocks, empty and full sets."""
+    rng = np.random.default_rng(V)
+    src = np.arange(V, dtype=np.int64)
+    g = gg.Graph.from_coo(V, src, src)
+    rt = gg.Runtime(gg.ExecConfig(), g)
+    for ids in (np.array([], np.int64), rng.integers(0, V, size=max(1, V // 3)),
+                np.arange(V), np.array([V - 1, 0, V - 1])):
+        fr = rt.frontiers.new_frontier(V, ids)
+        dense = fr.convert(target)
+        want = sorted(set(int(x) for x in ids))
+        assert dense.size == len(want)
+        assert dense.members() == want
+        back = dense.convert("SPARSE")
+        assert back.members() == want
+        assert back.size == len(want)
