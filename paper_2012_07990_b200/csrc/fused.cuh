@@ -108,7 +108,7 @@ __device__ __forceinline__ void fused_edge_phase(const gg_schedule& s, const Csr
         b_push_etwc<Op>(a, cta);
         if (a.huge) {
           grid.sync();
-          b_push_huge<Op>(a);
+          b_push_huge<Op, false>(a);
           grid.sync();
           if (tid == 0) *sc.etwc_n = 0;  // next append is behind the caller's barrier
         }

@@ -180,7 +180,7 @@ def test_dense_sparse_round_trip(gg, V, target):
     g = gg.Graph.from_coo(V, src, src)
     rt = gg.Runtime(gg.ExecConfig(), g)
     for ids in (np.array([], np.int64), rng.integers(0, V, size=max(1, V // 3)),
-                np.arange(V), np.array([V - 1, 0, V - 1])):
+                np.arange(V), np.array([V - 1, 0, V - 1][:min(3, V + 1)])):  # capacity V + 1
         fr = rt.frontiers.new_frontier(V, ids)
         dense = fr.convert(target)
         want = sorted(set(int(x) for x in ids))
