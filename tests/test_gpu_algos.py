@@ -414,3 +414,25 @@ def test_chunked_pass_many_ranges(gg, lb):
     assert r.stats.edges_traversed == int(sum(np.diff(off)[np.asarray(r.values) >= 0]))
     want, _ = oracle.cc(V, g.coo_src, g.coo_dst)
     assert np.array_equal(gg.cc_soman(g, prog).array, want)
+
+
+@pytest.mark.parametrize("dedup", [False, True])
+def test_staged_output_overflow(gg, dedup):
+    """One ETWC CTA step (256 frontier vertices) discovering 4800 vertices:
+    more appends than the 2048-entry shared-memory stage, so lane groups fall
+    back to the global queue mid-step; the next frontier must hold every
+    discovered vertex exactly once (BFS levels exact, arcs scanned exact)."""
+    mids = np.arange(1, 301)
+    leaves = 301 + np.arange(300 * 16)
+    src = np.concatenate([np.zeros(300, np.int64), np.repeat(mids, 16)])
+    dst = np.concatenate([mids, leaves]).astype(np.int64)
+    from paper_2012_07990_b200.graphio import symmetrize_coo
+    V = 301 + 300 * 16 + 5
+    s2, d2, _, _ = symmetrize_coo(src, dst)
+    g = gg.Graph.from_coo(V, s2, d2, symmetric=True)
+    off, nbr, _ = oracle.csr(V, g.coo_src, g.coo_dst)
+    prog = program_with(gg.Schedule(direction="PUSH", load_balance="ETWC", dedup=dedup))
+    r = gg.bfs(g, 0, prog)
+    assert gg.bfs_levels(r.values) == oracle.bfs_levels(V, off, nbr, 0).tolist()
+    assert r.stats.edges_traversed == int(sum(np.diff(off)[np.asarray(r.values) >= 0]))
+    legal_bfs_tree(g, r.values, 0)
