@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 240 python -m pytest tests/test_gpu_algos.py -q -x -p no:cacheprovider --timeout=60 --timeout-method=thread > gpurun_out/r78_tests.txt 2>&1 || exit 3
+timeout 300 python -m pytest tests -m gpu -q -x -p no:cacheprovider --timeout=60 --timeout-method=thread > gpurun_out/r78_all.txt 2>&1 || exit 4
+timeout 240 python bench.py --config c2 --check > gpurun_out/r78_c2.json 2> gpurun_out/r78_c2.err
+timeout 300 python bench.py --config c4 > gpurun_out/r78_c4.json 2> gpurun_out/r78_c4.err
