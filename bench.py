@@ -7,8 +7,17 @@ a/b/c = .57/.19/.19, seed 7), 20 iterations, tolerance 0.  One "step" = one
 complete ``pagerank(g, program, max_iters=20, tolerance=0.0)`` call with the
 graph resident in HBM; metric GTEPS = 20*E / step time.
 
+After the timed region (N = 1) the same run
+  * checks the RMAT-27 ranks against the CPU oracle (``parity``; the oracle's
+    20-iteration run on the host cores is also ``cpu_baseline``), and
+  * runs configs[0..3] (C1 PageRank RMAT-16, C2 DO-BFS RMAT-24, C3 fused
+    delta-SSSP 4096^2, C4 CC+BC Kronecker-25) in subprocesses
+    (``bench_algos.py``), each with its own roofline / e2e / cpu_baseline /
+    parity, nested under ``"configs"``.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gg|reference]
-                  [--config c5|c1|...] [--scale S] [--schedule eb|edge|pull|...]
+                  [--config c5|c1|c2|c3|c4] [--scale S] [--schedule eb|edge|pull|...]
+                  [--no-sub] [--no-parity]
 
 Multi-GPU (torchrun): the same RMAT-27 graph is 1-D partitioned by
 destination over the N ranks (EdgeBlocking layout per rank, NCCL allgather of
@@ -31,9 +40,9 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     # name: (scale, edge_factor, seed, iterations)
     "c5": (27, 16, 7, 20),
-    "c1": (16, 16, 1, 20),
 }
-ALGO_CONFIGS = ("c2", "c3", "c4")  # bench_algos.py: BFS / SSSP / CC+BC (configs[1..3])
+# bench_algos.py: PageRank RMAT-16 / BFS / SSSP / CC+BC (configs[0..3])
+ALGO_CONFIGS = ("c1", "c2", "c3", "c4")
 
 SCHEDULES = {
     "eb": dict(load_balance="EDGE_ONLY", blocking=True),
@@ -59,7 +68,6 @@ def parse():
     p.add_argument("--permute", action="store_true", help="Graph500-style id permutation")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-scale", type=int, default=22)
     # c2-c4 (bench_algos.py)
     p.add_argument("--sources", type=int, default=None)
     p.add_argument("--theta", type=float, default=0.0005, help="c2 hybrid threshold (swept: best)")
@@ -74,7 +82,9 @@ def parse():
     p.add_argument("--no-fusion", action="store_true", help="c3: unfused loop")
     p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED,EB,EDGE,HYBRID",
                    help="c4 load balances (EB = EDGE_ONLY+BLOCKED, EDGE = EDGE_ONLY)")
-    p.add_argument("--check", action="store_true", help="c2-c4: validate against the oracle")
+    p.add_argument("--no-sub", action="store_true", help="c5: skip the C1-C4 sub-runs")
+    p.add_argument("--no-parity", action="store_true", help="c5: skip the full-size oracle check")
+    p.add_argument("--sub-timeout", type=int, default=900)
     return p.parse_args()
 
 
@@ -137,30 +147,92 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port (test infrastructure) on the host cores
+# CPU side: the oracle port (test infrastructure) on the host cores -- the
+# full-size parity check and the CPU baseline of the same workload
 # ---------------------------------------------------------------------------
-def cpu_pagerank_sample(scale, edge_factor, seed, budget_s=20.0, max_iters=20):
-    import numpy as np
+def cpu_pagerank_full(V, src, dst, iters):
+    """oracle.c or_pagerank_par (pull over an OpenMP-built CSR-in, f64) on the
+    full graph: returns (ranks, seconds for the iterations, build seconds)."""
     import oracle
-    V, s, d = oracle.rmat(scale, edge_factor, seed=seed)
-    in_off, in_nbr, _ = oracle.csr(V, d, s)
-    out_off, _, _ = oracle.csr(V, s, np.zeros_like(d))
-    E = len(s)
-    # one warm-up iteration, then as many timed single-iteration steps as fit the budget
-    oracle.pagerank_par(V, in_off, in_nbr, out_off, 1, 0.0)
     t0 = time.perf_counter()
-    iters = 0
-    while iters < max_iters:
+    in_off, in_nbr, _ = oracle.csr_par(V, dst, src)
+    out_off = oracle.offsets_par(V, src)
+    build_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ranks, _ = oracle.pagerank_par(V, in_off, in_nbr, out_off, iters, 0.0)
+    return ranks, time.perf_counter() - t0, build_s
+
+
+def rel_err(got, want):
+    import numpy as np
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
+
+
+def reference_arm(args, metric, scale, ef, seed, iters, workload):
+    """--impl reference: the oracle port of the reference's PageRank on the
+    host cores, on THIS arm's graph (RMAT-27, generated on the host by the
+    bit-identical C replica of the device generator); one step = one
+    PageRank iteration over all 2^31 edges (a 20-iteration step would take
+    ~15 s x (K + W)); value = E / median step time."""
+    import oracle
+    t0 = time.perf_counter()
+    V, s, d = oracle.rmat(scale, ef, seed=seed)
+    in_off, in_nbr, _ = oracle.csr_par(V, d, s)
+    out_off = oracle.offsets_par(V, s)
+    del d
+    prep_s = time.perf_counter() - t0
+    E = len(s)
+    del s
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         oracle.pagerank_par(V, in_off, in_nbr, out_off, 1, 0.0)
-        iters += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": E * iters / dt / 1e9, "unit": "GTEPS", "cores": oracle.num_threads(),
-            "kind": "port",
-            "sample": "RMAT scale %d ef %d seed %d (E=%d), %d PageRank iteration(s) of "
-                      "oracle.c or_pagerank_par (pull, OpenMP, f64) in %.1f s"
-                      % (scale, edge_factor, seed, E, iters, dt)}
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    step_s = statistics.median(times)
+    v = E / step_s / 1e9
+    sample = ("full C5 graph (RMAT-27 ef16 seed 7, E=%d); oracle.c or_pagerank_par (pull over "
+              "CSR-in, OpenMP, f64): %d timed single-iteration steps after %d warm-up, median "
+              "%.3f s/iteration (graph generation + CSR build %.1f s, untimed)"
+              % (E, args.steps, args.warmup, step_s, prep_s))
+    return {"metric": metric, "value": v, "unit": "GTEPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload, "V": V, "E": E, "iterations_per_step": 1,
+                       "same_graph_as_gg_arm": True},
+            "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": oracle.num_threads(),
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def run_subconfigs(args, names):
+    """configs[0..3] in subprocesses (own CUDA context each; a failure or a
+    timeout is recorded, never fatal to the headline line)."""
+    out = {}
+    for name in names:
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", name,
+               "--steps", "5", "--warmup", "3"]
+        t0 = time.perf_counter()
+        try:
+            p = subprocess.run(cmd, capture_output=True, text=True, timeout=args.sub_timeout,
+                               cwd=ROOT)
+            lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+            if p.returncode == 0 and lines:
+                d = json.loads(lines[-1])
+                for k in ("metric", "n_gpus", "higher_is_better", "vs_baseline"):
+                    d.pop(k, None)
+                out[name] = d
+            else:
+                out[name] = {"error": "rc=%d" % p.returncode,
+                             "stderr_tail": p.stderr[-2000:]}
+        except subprocess.TimeoutExpired:
+            out[name] = {"error": "timeout after %d s" % args.sub_timeout}
+        out[name]["run_s"] = time.perf_counter() - t0
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -181,24 +253,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cs = min(args.cpu_scale, scale)
-        step_vals = []
-        for _ in range(args.warmup):
-            cpu_pagerank_sample(cs, ef, seed, budget_s=5.0, max_iters=1)
-        for _ in range(args.steps):
-            step_vals.append(cpu_pagerank_sample(cs, ef, seed, budget_s=10.0, max_iters=3))
-        v = statistics.median(x["value"] for x in step_vals)
-        base = step_vals[0]
-        line = {"metric": metric, "value": v, "unit": "GTEPS", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic", "impl": "reference",
-                "config": {"workload": workload, "cpu_sample_scale": cs, "iterations": iters},
-                "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": base["cores"],
-                                 "kind": "port", "sample": base["sample"]},
-                "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        print(json.dumps(reference_arm(args, metric, scale, ef, seed, iters, workload)))
         return
 
     import numpy as np
@@ -336,14 +391,17 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary()}
 
+    # device ranks of the last timed step (parity below, outside the timed region)
+    ranks_dev = ranks.cpu().numpy() if rank == 0 and world == 1 else None
+    src_h = torch.from_numpy(g.coo_src).pin_memory()
+    dst_h = torch.from_numpy(g.coo_dst).pin_memory()
+    g.close()
+    del g
+    torch.cuda.empty_cache()
+    ranks_h = torch.empty(V, dtype=torch.float64).pin_memory()
+
     # e2e: host COO in pinned memory -> Graph.from_coo -> pagerank -> ranks on host
     if not args.no_e2e:
-        src_h = torch.from_numpy(g.coo_src).pin_memory()
-        dst_h = torch.from_numpy(g.coo_dst).pin_memory()
-        g.close()
-        del g
-        torch.cuda.empty_cache()
-        ranks_h = torch.empty(V, dtype=torch.float64).pin_memory()
         e2e_steps = min(3, args.steps)
 
         def e2e_step():
@@ -372,10 +430,35 @@ def main():
                        "s_per_step": e2e_s,
                        "includes": "H2D of COO from pinned host memory, device graph build "
                                    "(EdgeBlocking prep), 20 iterations, D2H of ranks"}
-    if rank == 0 and world == 1 and not args.no_cpu:
-        # bounded sample: ~10 s of PageRank iterations on the host cores
-        line["cpu_baseline"] = cpu_pagerank_sample(min(args.cpu_scale, scale), ef, seed,
-                                                   budget_s=10.0, max_iters=10000)
+    if rank == 0 and world == 1:
+        from paper_2012_07990_b200 import _lib as L
+        L.load().gg_release_cached_memory()
+        torch.cuda.empty_cache()
+        if not (args.no_parity and args.no_cpu):
+            # the oracle's 20 iterations over the full graph: parity + CPU baseline
+            want, cpu_s, build_s = cpu_pagerank_full(V, src_h.numpy(), dst_h.numpy(), iters)
+            import oracle
+            if not args.no_parity:
+                line["parity"] = {
+                    "vs": "oracle.c or_pagerank_par (algos.py:163-208 restated; pull, f64), "
+                          "same RMAT-27 COO, %d iterations" % iters,
+                    "max_rel_err": rel_err(ranks_dev, want),
+                    "e2e_max_rel_err": rel_err(ranks_h.numpy(), want) if not args.no_e2e
+                    else None,
+                    "tolerance": 1e-6, "scale": scale}
+                line["parity"]["ok"] = max(line["parity"]["max_rel_err"],
+                                           line["parity"]["e2e_max_rel_err"] or 0.0) <= 1e-6
+            if not args.no_cpu:
+                line["cpu_baseline"] = {
+                    "value": iters * E / cpu_s / 1e9, "unit": "GTEPS",
+                    "cores": oracle.num_threads(), "kind": "port",
+                    "sample": "full C5 workload: oracle.c or_pagerank_par (pull over an OpenMP "
+                              "CSR-in, f64), RMAT-27, %d iterations in %.1f s (CSR build "
+                              "%.1f s untimed)" % (iters, cpu_s, build_s)}
+            del want
+        del src_h, dst_h, ranks_h
+        if not args.no_sub and args.config == "c5" and not args.scale:
+            line["configs"] = run_subconfigs(args, ("c1", "c2", "c3", "c4"))
     if rank == 0:
         print(json.dumps(line))
     if comm is not None:
@@ -385,8 +468,8 @@ def main():
 
 
 def main_algo(args, metric):
-    """configs[1..3]: one GPU (the north star keeps BFS-DO, SSSP, CC and BC
-    single-GPU); under torchrun rank 0 runs and the other ranks exit."""
+    """configs[0..3]: one GPU (the north star keeps BFS-DO, SSSP, CC and BC
+    single-GPU; C1 fits in L2); under torchrun rank 0 runs, the others exit."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     import bench_algos

@@ -143,3 +143,81 @@ def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1):
     d = np.empty(E, np.int32)
     L.or_rmat(scale, E, a, b, c, seed, _p(s), _p(d))
     return V, s, d
+
+
+# ---------------------------------------------------------------------------
+# full-scale parity helpers (OpenMP; see the oracle.c section header)
+# ---------------------------------------------------------------------------
+def _par_lib():
+    L = lib()
+    if not getattr(L, "_par_ready", False):
+        P, I64 = C.c_void_p, C.c_int64
+        L.or_offsets_par.argtypes = [I64, I64, P, P]
+        L.or_build_csr_par.argtypes = [I64, I64, P, P, P, P, P, P]
+        L.or_bfs_levels_do.restype = I64
+        L.or_bfs_levels_do.argtypes = [I64, P, P, P, P, I64, P]
+        L.or_bfs_check_tree.restype = I64
+        L.or_bfs_check_tree.argtypes = [I64, P, P, I64, P, P]
+        L.or_cc_par.restype = I64
+        L.or_cc_par.argtypes = [I64, I64, P, P, P]
+        L.or_bc_par.argtypes = [I64, P, P, P, P, P, I64, P]
+        L._par_ready = True
+    return L
+
+
+def offsets_par(V, keys):
+    keys = _c(keys, np.int32)
+    off = np.empty(V + 1, np.int64)
+    _par_lib().or_offsets_par(V, len(keys), _p(keys), _p(off))
+    return off
+
+
+def csr_par(V, keys, vals, w=None):
+    """CSR keys -> vals; neighbour order within a key unspecified."""
+    keys, vals = _c(keys, np.int32), _c(vals, np.int32)
+    E = len(keys)
+    off = np.empty(V + 1, np.int64)
+    nbr = np.empty(max(E, 1), np.int32)
+    wi = wout = None
+    if w is not None:
+        wi = _c(w, np.uint32)
+        wout = np.empty(max(E, 1), np.uint32)
+    _par_lib().or_build_csr_par(V, E, _p(keys), _p(vals), _p(wi), _p(off), _p(nbr), _p(wout))
+    return off, nbr[:E], (None if wout is None else wout[:E])
+
+
+def bfs_levels_do(V, off, nbr, source, in_off=None, in_nbr=None):
+    """Direction-optimising BFS levels (unique: equal to bfs_levels)."""
+    if in_off is None:
+        in_off, in_nbr = off, nbr
+    out = np.empty(V, np.int32)
+    _par_lib().or_bfs_levels_do(V, _p(_c(off, np.int64)), _p(_c(nbr, np.int32)),
+                                _p(_c(in_off, np.int64)), _p(_c(in_nbr, np.int32)), source,
+                                _p(out))
+    return out
+
+
+def bfs_check_tree(V, in_off, in_nbr, source, parents, levels):
+    """Number of vertices violating BFS-tree legality (0 = legal tree)."""
+    return int(_par_lib().or_bfs_check_tree(V, _p(_c(in_off, np.int64)), _p(_c(in_nbr, np.int32)),
+                                            source, _p(_c(parents, np.int32)),
+                                            _p(_c(levels, np.int32))))
+
+
+def cc_par(V, src, dst):
+    src, dst = _c(src, np.int32), _c(dst, np.int32)
+    out = np.empty(V, np.int32)
+    rounds = _par_lib().or_cc_par(V, len(src), _p(src), _p(dst), _p(out))
+    return out, rounds
+
+
+def bc_par(V, off, nbr, sources, in_off=None, in_nbr=None):
+    """in_off/in_nbr default to off/nbr (symmetric graphs, as bc requires)."""
+    if in_off is None:
+        in_off, in_nbr = off, nbr
+    src = _c(sources, np.int64)
+    out = np.empty(V, np.float64)
+    _par_lib().or_bc_par(V, _p(_c(off, np.int64)), _p(_c(nbr, np.int32)),
+                         _p(_c(in_off, np.int64)), _p(_c(in_nbr, np.int32)), _p(src), len(src),
+                         _p(out))
+    return out

@@ -371,3 +371,202 @@ void or_rmat(int scale, int64_t E, double a, double b, double c, uint64_t seed, 
     dst[i] = (int32_t)d;
   }
 }
+
+/* ------------------------------------------------------------------------
+ * Full-scale parity helpers (OpenMP).  Same results as the serial
+ * restatements above wherever the result is order-independent: CSR
+ * neighbour order within a vertex is unspecified (atomic scatter), BFS
+ * levels / CC canonical labels / SSSP distances are unique, and the BC and
+ * PageRank sums differ only in summation order (checked against the serial
+ * versions in tests/test_oracle_golden.py).  Used by bench.py's parity and
+ * cpu_baseline legs at the BASELINE sizes, where the serial ones take minutes.
+ * ------------------------------------------------------------------------ */
+
+/* offsets of a CSR keyed by keys[] (graphio.py:95-102, counts only) */
+void or_offsets_par(int64_t V, int64_t E, const int32_t* keys, int64_t* off) {
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v <= V; ++v) off[v] = 0;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < E; ++i) __atomic_fetch_add(&off[keys[i] + 1], 1, __ATOMIC_RELAXED);
+  for (int64_t v = 0; v < V; ++v) off[v + 1] += off[v];
+}
+
+/* CSR keys -> vals with neighbour order within a key unspecified. */
+void or_build_csr_par(int64_t V, int64_t E, const int32_t* keys, const int32_t* vals,
+                      const uint32_t* w, int64_t* off, int32_t* nbr, uint32_t* wout) {
+  or_offsets_par(V, E, keys, off);
+  int64_t* cur = (int64_t*)malloc((V + 1) * sizeof(int64_t));
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v <= V; ++v) cur[v] = off[v];
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < E; ++i) {
+    int64_t p = __atomic_fetch_add(&cur[keys[i]], 1, __ATOMIC_RELAXED);
+    nbr[p] = vals[i];
+    if (w && wout) wout[p] = w[i];
+  }
+  free(cur);
+}
+
+/* Direction-optimising BFS levels (top-down over a byte frontier, bottom-up
+ * over the in-adjacency when the frontier is large).  Levels are unique, so
+ * this equals or_bfs_levels for any switch rule.  Returns the level count. */
+int64_t or_bfs_levels_do(int64_t V, const int64_t* off, const int32_t* nbr,
+                         const int64_t* in_off, const int32_t* in_nbr, int64_t source,
+                         int32_t* level) {
+  uint8_t* cur = (uint8_t*)calloc(V > 0 ? V : 1, 1);
+  uint8_t* nxt = (uint8_t*)calloc(V > 0 ? V : 1, 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < V; ++v) level[v] = -1;
+  level[source] = 0;
+  cur[source] = 1;
+  int64_t nf = 1, d = 0;
+  while (nf) {
+    int64_t cnt = 0;
+    if (nf * 20 > V) { /* bottom-up */
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : cnt)
+      for (int64_t v = 0; v < V; ++v) {
+        if (level[v] != -1) continue;
+        for (int64_t e = in_off[v]; e < in_off[v + 1]; ++e)
+          if (cur[in_nbr[e]]) { level[v] = (int32_t)(d + 1); nxt[v] = 1; cnt++; break; }
+      }
+    } else { /* top-down */
+#pragma omp parallel for schedule(dynamic, 1024) reduction(+ : cnt)
+      for (int64_t u = 0; u < V; ++u) {
+        if (!cur[u]) continue;
+        for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+          int32_t v = nbr[e];
+          if (level[v] == -1 && __sync_bool_compare_and_swap(&level[v], -1, (int32_t)(d + 1))) {
+            nxt[v] = 1;
+            cnt++;
+          }
+        }
+      }
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < V; ++v) cur[v] = 0;
+    uint8_t* t = cur; cur = nxt; nxt = t;
+    nf = cnt;
+    d++;
+  }
+  free(cur);
+  free(nxt);
+  return d;
+}
+
+/* BFS parent-tree legality (test_algos.py:55-62): the
+ * source is its own parent, exactly the reached vertices have parents, each
+ * parent sits one level above its child and the arc parent->child exists
+ * (looked up in the child's in-adjacency).  Returns the number of
+ * violating vertices (0 = legal). */
+int64_t or_bfs_check_tree(int64_t V, const int64_t* in_off, const int32_t* in_nbr,
+                          int64_t source, const int32_t* parent, const int32_t* level) {
+  int64_t bad = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : bad)
+  for (int64_t v = 0; v < V; ++v) {
+    int32_t p = parent[v];
+    if (v == source) { bad += (p != source); continue; }
+    if (level[v] == -1) { bad += (p != -1); continue; }
+    if (p < 0 || p >= V || level[p] != level[v] - 1) { bad++; continue; }
+    int found = 0;
+    for (int64_t e = in_off[v]; e < in_off[v + 1] && !found; ++e) found = (in_nbr[e] == p);
+    bad += !found;
+  }
+  return bad;
+}
+
+/* cc_soman result (algos.py:267-307) by parallel hooking (atomic min on the
+ * higher label, as the reference's hook) + pointer jumping to a fixpoint;
+ * the canonical labels (component minimum id) are unique, so they equal
+ * or_cc's.  Returns the number of hooking rounds. */
+int64_t or_cc_par(int64_t V, int64_t E, const int32_t* src, const int32_t* dst, int32_t* out) {
+  int32_t* label = out;
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < V; ++v) label[v] = (int32_t)v;
+  int64_t rounds = 0;
+  int changed = 1;
+  while (changed) {
+    changed = 0;
+#pragma omp parallel for schedule(static) reduction(| : changed)
+    for (int64_t i = 0; i < E; ++i) {
+      int32_t la = label[src[i]], lb = label[dst[i]];
+      if (la == lb) continue;
+      int32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
+      int32_t cur = __atomic_load_n(&label[hi], __ATOMIC_RELAXED);
+      while (lo < cur) {
+        if (__atomic_compare_exchange_n(&label[hi], &cur, lo, 0, __ATOMIC_RELAXED,
+                                        __ATOMIC_RELAXED)) { changed = 1; break; }
+      }
+    }
+    int moved = 1;
+    while (moved) {
+      moved = 0;
+#pragma omp parallel for schedule(static) reduction(| : moved)
+      for (int64_t v = 0; v < V; ++v) {
+        int32_t l = label[v], ll = label[l];
+        if (ll != l) { label[v] = ll; moved = 1; }
+      }
+    }
+    rounds++;
+  }
+  return rounds; /* every label is now its component's minimum id (a root) */
+}
+
+/* bc (algos.py:314-395) level-synchronously in pull form: sigma[v] = sum of
+ * sigma over in-neighbours one level up, then
+ * delta[u] = sum over out-neighbours v one level down of sigma[u]/sigma[v]*(1+delta[v])
+ * — the same terms as the reference's push rounds (duplicates counted per
+ * arc), summed in a different order. */
+void or_bc_par(int64_t V, const int64_t* off, const int32_t* nbr, const int64_t* in_off,
+               const int32_t* in_nbr, const int64_t* sources, int64_t nsrc, double* score) {
+  int32_t* depth = (int32_t*)malloc((V > 0 ? V : 1) * sizeof(int32_t));
+  double* sigma = (double*)malloc((V > 0 ? V : 1) * sizeof(double));
+  double* delta = (double*)malloc((V > 0 ? V : 1) * sizeof(double));
+  int32_t* order = (int32_t*)malloc((V > 0 ? V : 1) * sizeof(int32_t));
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < V; ++v) score[v] = 0.0;
+  for (int64_t si = 0; si < nsrc; ++si) {
+    int64_t s = sources[si];
+    int64_t nl = or_bfs_levels_do(V, off, nbr, in_off, in_nbr, s, depth);
+    int64_t* start = (int64_t*)calloc(nl + 2, sizeof(int64_t));
+    for (int64_t v = 0; v < V; ++v)
+      if (depth[v] >= 0) start[depth[v] + 1]++;
+    for (int64_t l = 0; l < nl; ++l) start[l + 1] += start[l];
+    int64_t* cur = (int64_t*)malloc((nl + 1) * sizeof(int64_t));
+    memcpy(cur, start, (nl + 1) * sizeof(int64_t));
+    for (int64_t v = 0; v < V; ++v)
+      if (depth[v] >= 0) order[cur[depth[v]]++] = (int32_t)v;
+    free(cur);
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < V; ++v) { sigma[v] = 0.0; delta[v] = 0.0; }
+    sigma[s] = 1.0;
+    for (int64_t l = 1; l < nl; ++l) {
+#pragma omp parallel for schedule(dynamic, 256)
+      for (int64_t i = start[l]; i < start[l + 1]; ++i) {
+        int32_t v = order[i];
+        double sg = 0.0;
+        for (int64_t e = in_off[v]; e < in_off[v + 1]; ++e)
+          if (depth[in_nbr[e]] == l - 1) sg += sigma[in_nbr[e]];
+        sigma[v] = sg;
+      }
+    }
+    for (int64_t l = nl - 2; l >= 0; --l) {
+#pragma omp parallel for schedule(dynamic, 256)
+      for (int64_t i = start[l]; i < start[l + 1]; ++i) {
+        int32_t u = order[i];
+        double dl = 0.0;
+        for (int64_t e = off[u]; e < off[u + 1]; ++e) {
+          int32_t v = nbr[e];
+          if (depth[v] == l + 1) dl += sigma[u] / sigma[v] * (1.0 + delta[v]);
+        }
+        delta[u] = dl;
+      }
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t v = 0; v < V; ++v)
+      if (v != s) score[v] += delta[v];
+    free(start);
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t v = 0; v < V; ++v) score[v] /= 2.0;
+  free(depth); free(sigma); free(delta); free(order);
+}

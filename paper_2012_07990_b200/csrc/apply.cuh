@@ -10,11 +10,16 @@ void strict_prefix(Runtime* rt, const InView& in, int64_t n);
 void strict_spans(Runtime* rt, int64_t nspans);
 void clear_marks(Runtime* rt, Frontier* out, const OutBuilder& ob);
 Frontier* converted_view(Runtime* rt, Frontier* in, int repr);
-void twc_queues(Runtime* rt, TwcQueues* q);
-// ETWC huge-range queue (capacity E / kEtwcHuge + 1), count zeroed on the stream
-void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small_frontier = 0);
+// TWC bins sized for `entries` active-list entries (>= V; a multiset input may exceed V)
+void twc_queues(Runtime* rt, TwcQueues* q, int64_t entries = 0);
+// ETWC huge-range queue (capacity max(E / kEtwcHuge, small_frontier, entries) + 1),
+// count zeroed on the stream
+void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small_frontier = 0,
+               int64_t entries = 0);
 OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out);
 void dense_size_on_device(Frontier* f, cudaStream_t s);
+// sum of the out-degrees of the n entries of a SPARSE input (one round trip)
+int64_t degree_sum(Runtime* rt, const InView& in, int64_t n);
 
 template <class Op>
 void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, InView in,
@@ -42,7 +47,7 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
       // CTAs): all of them go to the chunk-balanced grid pass instead.  The
       // bound keeps the pass's per-CTA walk of the queue short.
       const bool small = work < kEtwcSmallPerSm * sm_count(dev);
-      etwc_huge(rt, &a.huge, &a.huge_n, small ? work : 0);
+      etwc_huge(rt, &a.huge, &a.huge_n, small ? work : 0, work);
       if (small && a.huge) a.huge_min = cta;
       k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
       if (a.huge) {
@@ -59,8 +64,8 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
     }
     case GG_LB_TWC: {
       TwcQueues q;
-      twc_queues(rt, &q);
-      etwc_huge(rt, &a.huge, &a.huge_n);  // hubs skip the bins (b_twc_bin)
+      twc_queues(rt, &q, work);
+      etwc_huge(rt, &a.huge, &a.huge_n, 0, work);  // hubs skip the bins (b_twc_bin)
       k_twc_bin<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q, cta);
       a.scanned = rt->scanned.p;
       k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
@@ -195,6 +200,20 @@ std::unique_ptr<Frontier> apply_op(Runtime* rt, const Op& op, bool use_filter,
       Frontier* sv = in->repr == GG_SPARSE ? in : converted(GG_SPARSE);
       iv = sv->view();
       n_host = frontier_size_raw(sv, rt->stream);
+      // a multiset input (dedup off upstream) may emit more than the output
+      // queue's max(V, E) + 1 slots: size it exactly when the bound allows it
+      if (out && ob.mode == GG_CREATE_FUSED && ob.dedup == DEDUP_NONE &&
+          !EmitsOncePerVertex<Op>::value && n_host > 1) {
+        const_cast<Graph*>(g)->ensure_out();
+        const int64_t cap = (int64_t)out->ids.n;
+        if ((double)n_host * (double)g->max_out_degree >= (double)cap) {
+          const int64_t need = degree_sum(rt, iv, n_host) + 1;
+          if (need > cap) {
+            out->ids.alloc(need);
+            ob.queue = out->ids.p;
+          }
+        }
+      }
     }
     if (n_host > 0) run_push(rt, s, op, use_filter, iv, n_host, ob);
   } else {

@@ -338,7 +338,8 @@ int64_t gg::pagerank_dist_run(gg_comm* c, const Graph& g, int64_t max_iters, dou
   GG_CUDA(cudaMemcpyAsync(bounds.data(), dbounds.p, (P + 1) * 8, cudaMemcpyDeviceToHost, st));
   GG_CUDA(cudaStreamSynchronize(st));
   const int64_t lo = bounds[me], hi = bounds[me + 1];
-  PullPlan* plan = pull_plan_for(g, kPieceEdges, lo, hi);
+  std::shared_ptr<PullPlan> plan_hold = pull_plan_for(g, kPieceEdges, lo, hi);
+  PullPlan* plan = plan_hold.get();
   const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
   DevBuf<double> rank(V), scal(2 * (iters_cap + 2)), hubsum(V);
   DevBuf<CT> contrib0(V), contrib1(V);

@@ -387,7 +387,8 @@ __global__ void k_check_ids(const int32_t* ids, int64_t n, int64_t V, int* bad) 
 
 std::unique_ptr<Frontier> Runtime::new_frontier(const int32_t* ids, int64_t n) {
   auto f = acquire(GG_SPARSE);
-  if (n > (int64_t)f->ids.n) fail(GG_ERR_ENGINE, "frontier larger than its capacity");
+  // a user multiset may be longer than max(V, E) + 1 (frontier.py accepts any)
+  if (n > (int64_t)f->ids.n) f->ids.alloc(n);
   cudaPointerAttributes at{};
   bool host = true;
   if (cudaPointerGetAttributes(&at, ids) == cudaSuccess) host = at.type == cudaMemoryTypeUnregistered || at.type == cudaMemoryTypeHost;
@@ -602,7 +603,8 @@ void pool_free(void* q, size_t granted) {
   cudaSetDevice(cur);
 }
 
-void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small_frontier) {
+void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small_frontier,
+               int64_t entries) {
   rt->g->ensure_out();
   // no hub and a frontier that fills the grid: no grid pass (no extra barriers)
   if (rt->g->max_out_degree < kEtwcHuge && (small_frontier == 0 || rt->g->max_out_degree < rt->cfg.cta_size)) {
@@ -610,8 +612,9 @@ void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small
     *n = nullptr;
     return;
   }
-  // one entry per active vertex at most; per kEtwcHuge arcs for the hub pass
-  const int64_t cap = std::max(rt->g->E / kEtwcHuge, small_frontier) + 1;
+  // one entry per active-list entry at most (a multiset frontier -- dedup
+  // off -- repeats a hub once per occurrence), per kEtwcHuge arcs otherwise
+  const int64_t cap = std::max({rt->g->E / kEtwcHuge, small_frontier, entries}) + 1;
   if (rt->etwc_q.n < (size_t)cap) rt->etwc_q.alloc(cap);
   if (!rt->etwc_n.p) rt->etwc_n.alloc(1);
   GG_CUDA(cudaMemsetAsync(rt->etwc_n.p, 0, sizeof(unsigned long long), rt->stream));
@@ -671,6 +674,30 @@ __global__ void k_clear_marks(const int32_t* ids, const unsigned long long* n, u
 }
 
 
+__global__ void k_degree_sum(const InView in, const int64_t* off, int64_t n,
+                             unsigned long long* sum) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t u = active_at(in, i);
+    s += (unsigned long long)(off[u + 1] - off[u]);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(sum, s);
+}
+
+int64_t degree_sum(Runtime* rt, const InView& in, int64_t n) {
+  DevBuf<unsigned long long> d(1);
+  d.zero(rt->stream);
+  k_degree_sum<<<grid_for(n, 256, rt->dev), 256, 0, rt->stream>>>(in, rt->g->out_view().off, n, d.p);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  unsigned long long h = 0;
+  GG_CUDA(cudaMemcpyAsync(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost, rt->stream));
+  GG_CUDA(cudaStreamSynchronize(rt->stream));
+  return (int64_t)h;
+}
+
 void strict_prefix(Runtime* rt, const InView& in, int64_t n) {
   cudaStream_t st = rt->stream;
   rt->prefix.alloc(n + 1);
@@ -709,12 +736,14 @@ Frontier* converted_view(Runtime* rt, Frontier* in, int repr) {
   return rt->conv.get();
 }
 
-void twc_queues(Runtime* rt, TwcQueues* q) {
-  const int64_t V = rt->g->V;
-  if (rt->twc_q.n < (size_t)(3 * V + 3)) rt->twc_q.alloc(3 * V + 3);
+void twc_queues(Runtime* rt, TwcQueues* q, int64_t entries) {
+  // every active-list entry lands in one bin: a bin holds up to max(V,
+  // entries) ids (entries > V for a multiset SPARSE input, dedup off)
+  const int64_t cap = std::max(rt->g->V, entries) + 1;
+  if (rt->twc_q.n < (size_t)(3 * cap)) rt->twc_q.alloc(3 * cap);
   if (!rt->twc_cnt.p) rt->twc_cnt.alloc(3);
   GG_CUDA(cudaMemsetAsync(rt->twc_cnt.p, 0, 3 * 8, rt->stream));
-  *q = TwcQueues{{rt->twc_q.p, rt->twc_q.p + V + 1, rt->twc_q.p + 2 * (V + 1)}, rt->twc_cnt.p};
+  *q = TwcQueues{{rt->twc_q.p, rt->twc_q.p + cap, rt->twc_q.p + 2 * cap}, rt->twc_cnt.p};
 }
 
 OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out) {

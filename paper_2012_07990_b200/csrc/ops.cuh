@@ -10,6 +10,13 @@
 
 namespace gg {
 
+// Ops whose push emits a destination only on winning a CAS on its state
+// (at most once per vertex per apply): their SPARSE output never exceeds V,
+// whatever the input multiplicity.  Every other op may emit once per scanned
+// arc, so a multiset input can need more than max(V, E) + 1 output slots.
+template <class Op>
+struct EmitsOncePerVertex { static constexpr bool value = false; };
+
 template <class T>
 __device__ __forceinline__ T shfl_xor_any(T v, int o) {
   return __shfl_xor_sync(0xffffffffu, v, o);
@@ -44,6 +51,9 @@ struct OpBfs {
     }
   }
 };
+
+template <>
+struct EmitsOncePerVertex<OpBfs> { static constexpr bool value = true; };
 
 // Test UDF: in-degree counting from the active set (test_engine.py:246-264).
 struct OpCount {

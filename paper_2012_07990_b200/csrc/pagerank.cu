@@ -145,7 +145,8 @@ static int64_t pagerank_pull_wm(const Graph& g, bool fusion, int64_t max_iters, 
   const int64_t V = g.V;
   const int dev = g.dev;
   cudaStream_t st = rt.stream;
-  PullPlan* plan = pull_plan_for(g, kPieceEdges);
+  std::shared_ptr<PullPlan> plan_hold = pull_plan_for(g, kPieceEdges);
+  PullPlan* plan = plan_hold.get();
   CsrView in = g.in_view();
   DevBuf<CT> contrib1(V);
   DevBuf<double> hubsum(V);

@@ -277,16 +277,22 @@ static std::shared_ptr<PrBlockLayout> build_layout(const Graph& g, int64_t ns, i
   return L;
 }
 
-// cached on the graph (one layout per (window, contrib width, partition))
-static PrBlockLayout* layout_for(const Graph& gc, int64_t ns, int ct_bytes, PrPart part = PrPart()) {
+// cached on the graph (one layout per (window, contrib width, partition)).
+// Callers hold the returned shared_ptr for the whole query: a concurrent
+// query on the same graph that needs another layout replaces the cache
+// entry, and the old layout (its buffers and its w_mu) lives until its last
+// user returns.
+static std::shared_ptr<PrBlockLayout> layout_for(const Graph& gc, int64_t ns, int ct_bytes,
+                                                 PrPart part = PrPart()) {
   Graph& g = const_cast<Graph&>(gc);
   std::lock_guard<std::mutex> lk(g.mu);
-  auto* cur = static_cast<PrBlockLayout*>(g.pr_block.get());
+  auto cur = std::static_pointer_cast<PrBlockLayout>(g.pr_block);
   if (cur && cur->ns == ns && cur->ct_bytes == ct_bytes && cur->P == part.P && cur->r == part.r) return cur;
-  g.pr_block.reset();  // free the previous layout before building another
+  cur.reset();
+  g.pr_block.reset();  // drop the cache's reference before building another
   auto L = build_layout(g, ns, ct_bytes, part);
   g.pr_block = L;
-  return L.get();
+  return L;
 }
 
 int64_t pr_block_window(const Graph& g, int ct_bytes, int64_t blocking_size) {
@@ -309,8 +315,7 @@ int64_t pr_block_window(const Graph& g, int ct_bytes, int64_t blocking_size) {
 }
 
 double pr_block_prep_ms(const Graph& g, int64_t blocking_size, int ct_bytes) {
-  PrBlockLayout* L = layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes);
-  return L->prep_ms;
+  return layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes)->prep_ms;
 }
 
 template <class CT>
@@ -861,7 +866,9 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   const int dev = g.dev;
   const int64_t V = g.V;
   cudaStream_t st = rt.stream;
-  PrBlockLayout* L = layout_for(g, pr_block_window(g, sizeof(CT), s.blocking_size), sizeof(CT));
+  std::shared_ptr<PrBlockLayout> Lp =
+      layout_for(g, pr_block_window(g, sizeof(CT), s.blocking_size), sizeof(CT));
+  PrBlockLayout* L = Lp.get();
   const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
   std::lock_guard<std::mutex> wlk(L->w_mu);
   PrRank<CT> R;
@@ -1081,7 +1088,8 @@ int64_t pagerank_blocked_rank(const Graph& g, const gg_schedule& s, int P, int r
                               int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
                               int64_t* local_edges) {
   const int64_t ns = pr_block_window(g, sizeof(CT), s.blocking_size);
-  PrBlockLayout* L = layout_for(g, ns, sizeof(CT), PrPart{P, r});
+  std::shared_ptr<PrBlockLayout> Lp = layout_for(g, ns, sizeof(CT), PrPart{P, r});
+  PrBlockLayout* L = Lp.get();
   const int64_t iters_cap = max_iters > 0 ? max_iters : 0;
   std::lock_guard<std::mutex> wlk(L->w_mu);
   PrRank<CT> R;
@@ -1104,7 +1112,8 @@ template int64_t pagerank_blocked_rank<float>(const Graph&, const gg_schedule&, 
 
 double pr_block_prep_part_ms(const Graph& g, int64_t blocking_size, int ct_bytes, int P, int r,
                              int64_t* bounds, int32_t* newid) {
-  PrBlockLayout* L = layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes, PrPart{P, r});
+  std::shared_ptr<PrBlockLayout> L =
+      layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes, PrPart{P, r});
   if (bounds) memcpy(bounds, L->bounds.data(), (P + 1) * sizeof(int64_t));
   if (newid) GG_CUDA(cudaMemcpy(newid, L->newid.p, L->V * sizeof(int32_t), cudaMemcpyDefault));
   return L->prep_ms;

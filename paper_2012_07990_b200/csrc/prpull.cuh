@@ -79,12 +79,15 @@ static __global__ void k_plan_pad(int64_t first, int64_t nvrows, int64_t E, int6
 }
 
 // Plan over destination rows [lo, hi) (a rank's partition, or all rows).
-inline PullPlan* pull_plan_for(const Graph& gc, int64_t hub_t, int64_t lo = 0, int64_t hi = -1) {
+// Callers hold the returned shared_ptr for the query (a concurrent query may
+// replace the cache entry; the plan it uses stays alive).
+inline std::shared_ptr<PullPlan> pull_plan_for(const Graph& gc, int64_t hub_t, int64_t lo = 0,
+                                               int64_t hi = -1) {
   Graph& g = const_cast<Graph&>(gc);
   if (hi < 0) hi = g.V;
   std::lock_guard<std::mutex> lk(g.mu);
   if (g.pull_plan && g.pull_plan->hub_t == hub_t && g.pull_plan->lo == lo && g.pull_plan->hi == hi)
-    return g.pull_plan.get();
+    return g.pull_plan;
   CsrView in = g.in_view();
   in.off += lo;
   const int dev = g.dev;
@@ -121,7 +124,7 @@ inline PullPlan* pull_plan_for(const Graph& gc, int64_t hub_t, int64_t lo = 0, i
   GG_CUDA(cudaMemcpy(&h, nh.p, 8, cudaMemcpyDeviceToHost));
   p->nhubs = (int64_t)h;
   g.pull_plan = p;
-  return p.get();
+  return p;
 }
 
 static __global__ void k_outdeg(const int64_t* off, int64_t V, int32_t* deg) {

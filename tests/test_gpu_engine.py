@@ -180,7 +180,8 @@ def test_dense_sparse_round_trip(gg, V, target):
     g = gg.Graph.from_coo(V, src, src)
     rt = gg.Runtime(gg.ExecConfig(), g)
     for ids in (np.array([], np.int64), rng.integers(0, V, size=max(1, V // 3)),
-                np.arange(V), np.array([V - 1, 0, V - 1][:min(3, V + 1)])):  # capacity V + 1
+                np.arange(V), np.array([V - 1, 0, V - 1]),
+                rng.integers(0, V, size=3 * V + 5)):  # multisets longer than max(V, E) + 1
         fr = rt.frontiers.new_frontier(V, ids)
         dense = fr.convert(target)
         want = sorted(set(int(x) for x in ids))
@@ -189,3 +190,48 @@ def test_dense_sparse_round_trip(gg, V, target):
         back = dense.convert("SPARSE")
         assert back.members() == want
         assert back.size == len(want)
+
+
+def _hub_graph(gg, deg):
+    """hub 0 -> 1..deg and every leaf -> 0 (V = deg + 1, E = 2 deg)."""
+    leaves = np.arange(1, deg + 1, dtype=np.int64)
+    src = np.concatenate([np.zeros(deg, np.int64), leaves])
+    dst = np.concatenate([leaves, np.zeros(deg, np.int64)])
+    return gg.Graph.from_coo(deg + 1, src, dst)
+
+
+@pytest.mark.parametrize("lb", ["ETWC", "TWC", "STRICT", "CM", "WM", "VERTEX_BASED"])
+def test_push_over_multiset_with_hub(gg, torch, lb):
+    """A dedup-off EnqueueDst apply turns 20000 leaves into the hub repeated
+    20000 times (a multiset, frontier.py:160-161); every PUSH balancer then
+    walks the hub's 20000 arcs once per occurrence (the hub is past the
+    16384-arc grid-pass bound, so ETWC/TWC queue it once per occurrence)."""
+    deg = 20000
+    g = _hub_graph(gg, deg)
+    rt = gg.Runtime(gg.ExecConfig(), g)
+    leaves = rt.frontiers.new_frontier(deg + 1, list(range(1, deg + 1)))
+    hubs = gg.edgeset_apply(g, leaves, gg.udfs.EnqueueDst(), runtime=rt,
+                            schedule=gg.Schedule(dedup=False))
+    assert hubs.size == deg
+    counts = torch.zeros(deg + 1, dtype=torch.int64, device="cuda")
+    gg.edgeset_apply(g, hubs, gg.udfs.CountInDegree(counts), runtime=rt, collect_output=False,
+                     schedule=gg.Schedule(direction="PUSH", load_balance=lb))
+    c = counts.cpu().numpy()
+    assert c[0] == 0 and np.all(c[1:] == deg)
+    assert rt.stats.edges_traversed == deg + deg * deg
+
+
+@pytest.mark.parametrize("lb", ["ETWC", "TWC", "VERTEX_BASED"])
+def test_multiset_output_larger_than_edge_count(gg, lb):
+    """[hub] * 1000 with dedup off emits 1000 * deg entries, more than the
+    default max(V, E) + 1 output slots: the queue is sized from the input."""
+    deg = 100
+    g = _hub_graph(gg, deg)
+    rt = gg.Runtime(gg.ExecConfig(), g)
+    fr = rt.frontiers.new_frontier(deg + 1, [0] * 1000)
+    assert fr.size == 1000
+    out = gg.edgeset_apply(g, fr, gg.udfs.EnqueueDst(), runtime=rt,
+                           schedule=gg.Schedule(direction="PUSH", load_balance=lb, dedup=False))
+    assert out.size == 1000 * deg
+    m = np.bincount(np.asarray(out.members()), minlength=deg + 1)
+    assert m[0] == 0 and np.all(m[1:] == 1000)

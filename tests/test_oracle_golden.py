@@ -163,3 +163,69 @@ def test_oracle_scale16_bc(s16):
     off, nbr, _ = _csr(V, ss, dd)
     got = oracle.bc(V, off, nbr, [int(x) for x in s16["bc_sources"]])
     assert max_rel_err(got[s16["bc_scores"] > 1e-6], s16["bc_scores"][s16["bc_scores"] > 1e-6]) < 1e-9
+
+
+# ---------------------------------------------------------------------------
+# the OpenMP full-scale helpers (bench.py parity legs) against the same pins
+# ---------------------------------------------------------------------------
+def test_oracle_par_helpers_match_reference(golden_small):
+    seen = {"bfs": 0, "cc": 0, "bc": 0}
+    for case in golden_small["cases"]:
+        algo = case["algo"]
+        if algo not in seen:
+            continue
+        V, s, d, _ = arrays(golden_small["graphs"][case["graph"]])
+        off, nbr, _ = oracle.csr_par(V, s, d)
+        ref_off, ref_nbr, _ = _csr(V, s, d)
+        assert np.array_equal(off, ref_off)
+        for v in range(V):  # same multiset of neighbours per vertex
+            assert sorted(nbr[off[v]:off[v + 1]]) == sorted(ref_nbr[off[v]:off[v + 1]])
+        if algo == "bfs":
+            in_off, in_nbr, _ = oracle.csr_par(V, d, s)
+            lv = oracle.bfs_levels_do(V, off, nbr, case["source"], in_off, in_nbr)
+            assert lv.tolist() == case["levels"]
+            # a legal tree built from the levels passes; a corrupted one fails
+            par = np.full(V, -1, np.int32)
+            par[case["source"]] = case["source"]
+            for u in range(V):
+                for e in range(off[u], off[u + 1]):
+                    v = nbr[e]
+                    if lv[v] == lv[u] + 1 and par[v] == -1:
+                        par[v] = u
+            assert oracle.bfs_check_tree(V, in_off, in_nbr, case["source"], par, lv) == 0
+            reached = np.flatnonzero((lv > 0))
+            if len(reached):
+                bad = par.copy()
+                bad[reached[0]] = reached[0]
+                assert oracle.bfs_check_tree(V, in_off, in_nbr, case["source"], bad, lv) >= 1
+        elif algo == "cc":
+            labels, _ = oracle.cc_par(V, s, d)
+            assert labels.tolist() == case["labels"]
+        else:
+            in_off, in_nbr, _ = oracle.csr_par(V, d, s)
+            got = oracle.bc_par(V, off, nbr, case["sources"], in_off, in_nbr)
+            assert np.max(np.abs(got - np.asarray(case["scores"]))) < 1e-9
+        seen[algo] += 1
+    assert min(seen.values()) > 5
+
+
+def test_oracle_par_helpers_scale16(s16):
+    V, s, d = gen.rmat(16, 16, seed=2)
+    ss, dd = _sym(V, s, d)
+    off, nbr, _ = oracle.csr_par(V, ss, dd)
+    src = int(s16["bfs_source"])
+    assert np.array_equal(oracle.bfs_levels_do(V, off, nbr, src), s16["bfs_levels"])
+    labels, _ = oracle.cc_par(V, ss, dd)
+    assert np.array_equal(labels, s16["cc_labels"])
+    V, s, d = gen.rmat(13, 8, seed=6)
+    ss, dd = _sym(V, s, d)
+    off, nbr, _ = oracle.csr_par(V, ss, dd)
+    got = oracle.bc_par(V, off, nbr, [int(x) for x in s16["bc_sources"]])
+    m = s16["bc_scores"] > 1e-6
+    assert max_rel_err(got[m], s16["bc_scores"][m]) < 1e-9
+    # PageRank over the unordered CSR-in equals the COO-order restatement
+    V, s, d = gen.rmat(14, 8, seed=1)
+    in_off, in_nbr, _ = oracle.csr_par(V, d, s)
+    pr, _ = oracle.pagerank_par(V, in_off, in_nbr, oracle.offsets_par(V, s), 20, 0.0)
+    want, _ = oracle.pagerank(V, s, d, 20, 0.0)
+    assert max_rel_err(pr, want) < 1e-12
