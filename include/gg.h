@@ -203,22 +203,76 @@ int gg_frontier_convert(gg_runtime* rt, gg_frontier* f, int32_t repr, gg_frontie
 
 /* ---- edgeset.apply with a named device UDF (engine.py:418-460) ------------
  * The reference accepts an arbitrary Python udf(ctx); on the device each udf
- * is a named functor (SURVEY §7 hard part 1).  udf ids:
- *   GG_UDF_BFS       state: int32 parent[V]        push CAS / pull store + enqueue,
- *                                                   filter parent[v] == -1 (algos.py:114-125)
- *   GG_UDF_COUNT     state: int64 counts[V]         atomic_add(counts[dst], 1)
- *   GG_UDF_ENQUEUE   no state                       enqueue(dst)
- *   GG_UDF_PR        state: double acc[V], contrib  atomic_add(acc[dst], contrib[src]) (algos.py:180-181)
- * `filter` 0 = none, 1 = the udf's own filter.  device pointers in state. */
-enum { GG_UDF_BFS = 0, GG_UDF_COUNT = 1, GG_UDF_ENQUEUE = 2, GG_UDF_PR = 3 };
+ * is a named functor (SURVEY §7 hard part 1) -- every UDF the reference's
+ * algorithms define is one.  udf ids (state fields are device pointers):
+ *   GG_UDF_BFS        arr0 int32 parent[V]       push CAS / pull store + enqueue,
+ *                                                 filter parent[v] == -1 (algos.py:114-125)
+ *   GG_UDF_COUNT      arr0 int64 counts[V]       atomic_add(counts[dst], 1)
+ *   GG_UDF_ENQUEUE    -                          enqueue(dst)
+ *   GG_UDF_PR         arr0 double acc[V],        atomic_add(acc[dst], contrib[src]) (algos.py:180-181)
+ *                     arr1 double contrib[V]
+ *   GG_UDF_CC_HOOK    arr0 int32 label[V],       la, lb = label[src], label[dst];
+ *                     arr1 int changed            atomic_min(label, max, min) -> changed = 1
+ *                                                 (algos.py:283-293)
+ *   GG_UDF_BC_FORWARD arr0 int32 depth[V],       CAS depth -1 -> level+1 + enqueue; sigma[dst] +=
+ *                     arr1 double sigma[V],       sigma[src] when depth[dst] == level+1; filter
+ *                     i0 level                    depth == -1 or level+1 (algos.py:353-365)
+ *   GG_UDF_BC_BACKWARD arr0 depth, arr1 sigma,   delta[src] += sigma[src]/sigma[dst]*(1+delta[dst])
+ *                     arr2 double delta[V]        when depth[dst] == depth[src]+1 (algos.py:378-382)
+ *   GG_UDF_SSSP_RELAX arr0 gg_bucket_queue*      q.update_priority_min(dst, prio[src] + w)
+ *                                                 (algos.py:233-234)
+ * `filter` 0 = none, 1 = the udf's own filter. */
+enum {
+  GG_UDF_BFS = 0, GG_UDF_COUNT = 1, GG_UDF_ENQUEUE = 2, GG_UDF_PR = 3, GG_UDF_CC_HOOK = 4,
+  GG_UDF_BC_FORWARD = 5, GG_UDF_BC_BACKWARD = 6, GG_UDF_SSSP_RELAX = 7
+};
 typedef struct {
   void* arr0;
   void* arr1;
   int64_t i0;
+  void* arr2;
 } gg_udf_state;
 int gg_edgeset_apply(gg_runtime* rt, int32_t udf, const gg_udf_state* state, int32_t filter,
                      gg_frontier* input /* NULL = all vertices */, const gg_binding* binding,
                      int32_t reuse, int32_t collect_output, gg_frontier** out);
+
+/* engine.fused_loop / Runtime.fused_dispatch (engine.py:639-662,
+ * runtime.py:194-209): enter = 1 opens a fused region (one dispatch for
+ * everything inside, counted now), enter = 0 closes it; add_rounds adds loop
+ * bodies to RunStats.rounds. */
+int gg_runtime_fused_region(gg_runtime* rt, int32_t enter);
+int gg_runtime_add_rounds(gg_runtime* rt, int64_t n);
+
+/* ---- BucketQueue on the device (priority.py:17-118) --------------------------
+ * Priorities u64 (GG_UNREACHED = 2^64-1), current / far buckets as SPARSE
+ * queues with the reference's dedup (per round for current, until advance
+ * for far).  take_current hands out the current bucket as a frontier (input
+ * of a GG_UDF_SSSP_RELAX apply), recycle returns its storage.  advance
+ * reports *nonempty = 0 when drained (the reference returns None) and fails
+ * with GG_ERR_ENGINE while current is non-empty. */
+typedef struct gg_bucket_queue gg_bucket_queue;
+int gg_bucket_queue_create(int32_t device, int64_t universe, uint64_t delta,
+                           gg_bucket_queue** out);
+int gg_bucket_queue_destroy(gg_bucket_queue* q);
+int gg_bucket_queue_seed(gg_bucket_queue* q, int64_t v, uint64_t priority);
+int gg_bucket_queue_update_min(gg_bucket_queue* q, int64_t v, uint64_t candidate,
+                               int32_t* improved);
+int gg_bucket_queue_take_current(gg_bucket_queue* q, gg_frontier** taken);
+int gg_bucket_queue_recycle(gg_bucket_queue* q, gg_frontier* taken);
+int gg_bucket_queue_advance(gg_bucket_queue* q, int32_t* nonempty);
+int gg_bucket_queue_info(gg_bucket_queue* q, uint64_t* index, int64_t* current_size,
+                         int64_t* far_size);
+int gg_bucket_queue_members(gg_bucket_queue* q, int32_t which /* 0 current, 1 far */,
+                            int32_t* out, int64_t cap, int64_t* n);
+int gg_bucket_queue_priorities(gg_bucket_queue* q, uint64_t* out /* V, host or device */);
+
+/* ---- EdgeBlocking apply (blocking.py:116-186) -------------------------------
+ * Alg. 2 over the graph's blocked layout of width n (built and cached on
+ * first use, or installed from a sidecar): segments in order, each split
+ * evenly over the grid, a grid barrier between segments, the named udf's
+ * atomic form per edge; one dispatch.  *edges = edges processed. */
+int gg_apply_blocked(gg_runtime* rt, int64_t n, int32_t udf, const gg_udf_state* state,
+                     int64_t* edges);
 
 /* ---- algorithm drivers (algos.py) ------------------------------------------
  * fusion = the "s0" loop binding's kernel fusion (engine.fused_loop).  All

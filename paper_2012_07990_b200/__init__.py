@@ -12,8 +12,8 @@ from .frontier import BITMAP, BOOLMAP, SPARSE, FrontierError, VertexSubset
 from .graphio import (Graph, GraphLoadError, generate_grid, generate_kronecker, generate_rmat,
                       load_edge_list, load_graph, load_matrix_market, out_degree,
                       with_random_weights)
-from .priority import UNREACHED
-from .blocking import BlockedGraph, block_edges, default_blocking_size
+from .priority import UNREACHED, BucketQueue
+from .blocking import BlockedGraph, apply_blocked, block_edges, default_blocking_size
 from .engine import edgeset_apply, fused_loop, hybrid_apply
 from .algos import (ALGO_LABELS, ALGO_NAMES, AlgoResult, bc, bfs, bfs_levels, cc_soman,
                     pagerank, sssp_delta)
@@ -23,7 +23,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ALGO_LABELS", "ALGO_NAMES", "AlgoResult", "bc", "bfs", "bfs_levels", "cc_soman",
-    "pagerank", "sssp_delta", "BlockedGraph", "block_edges", "default_blocking_size",
+    "pagerank", "sssp_delta", "BlockedGraph", "apply_blocked", "block_edges",
+    "default_blocking_size", "BucketQueue",
     "BITMAP", "BOOLMAP", "SPARSE", "VertexSubset", "FrontierError", "Graph", "GraphLoadError",
     "load_edge_list", "load_graph", "load_matrix_market", "out_degree", "with_random_weights", "generate_rmat",
     "generate_grid", "generate_kronecker", "UNREACHED", "EdgeContext", "EngineError",

@@ -28,6 +28,7 @@ GG_ERR_FRONTIER = -6
 GG_ERR_OOM = -7
 
 UDF_BFS, UDF_COUNT, UDF_ENQUEUE, UDF_PR = 0, 1, 2, 3
+UDF_CC_HOOK, UDF_BC_FORWARD, UDF_BC_BACKWARD, UDF_SSSP_RELAX = 4, 5, 6, 7
 
 
 class GGSchedule(C.Structure):
@@ -67,7 +68,8 @@ class GGDeviceInfo(C.Structure):
 
 
 class GGUdfState(C.Structure):
-    _fields_ = [("arr0", C.c_void_p), ("arr1", C.c_void_p), ("i0", C.c_int64)]
+    _fields_ = [("arr0", C.c_void_p), ("arr1", C.c_void_p), ("i0", C.c_int64),
+                ("arr2", C.c_void_p)]
 
 
 VP = C.c_void_p
@@ -106,6 +108,19 @@ SIGNATURES = {
     "gg_frontier_convert": (I32, [VP, VP, I32, PP]),
     "gg_edgeset_apply": (I32, [VP, I32, C.POINTER(GGUdfState), I32, VP,
                                C.POINTER(GGBinding), I32, I32, PP]),
+    "gg_runtime_fused_region": (I32, [VP, I32]),
+    "gg_runtime_add_rounds": (I32, [VP, I64]),
+    "gg_bucket_queue_create": (I32, [I32, I64, U64, PP]),
+    "gg_bucket_queue_destroy": (I32, [VP]),
+    "gg_bucket_queue_seed": (I32, [VP, I64, U64]),
+    "gg_bucket_queue_update_min": (I32, [VP, I64, U64, C.POINTER(I32)]),
+    "gg_bucket_queue_take_current": (I32, [VP, PP]),
+    "gg_bucket_queue_recycle": (I32, [VP, VP]),
+    "gg_bucket_queue_advance": (I32, [VP, C.POINTER(I32)]),
+    "gg_bucket_queue_info": (I32, [VP, C.POINTER(U64), C.POINTER(I64), C.POINTER(I64)]),
+    "gg_bucket_queue_members": (I32, [VP, I32, VP, I64, C.POINTER(I64)]),
+    "gg_bucket_queue_priorities": (I32, [VP, VP]),
+    "gg_apply_blocked": (I32, [VP, I64, I32, C.POINTER(GGUdfState), C.POINTER(I64)]),
     "gg_bfs": (I32, [VP, I64, C.POINTER(GGBinding), I32, C.POINTER(GGExec), VP,
                      C.POINTER(GGStats)]),
     "gg_pagerank": (I32, [VP, C.POINTER(GGBinding), I32, C.POINTER(GGExec), I64, F64, F64,

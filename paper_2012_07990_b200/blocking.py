@@ -56,6 +56,7 @@ class BlockedGraph:
         self.edges_dst = edges_dst
         self.edges_weight = edges_weight
         self.prep_ms = prep_ms
+        self.graph = None  # the device Graph whose cached layout this is
 
     def segment_range(self, s):
         lo = self.segment_start[s - 1] if s else 0
@@ -89,11 +90,43 @@ def block_edges(g, n):
         w = np.empty(max(E, 1), np.uint32)
         _lib.call("gg_blocked_copy_array", h, 3, _lib.ptr(w))
         w = w[:E].astype(np.int64).tolist()
-    return BlockedGraph(g.num_vertices, n, seg[:nseg.value].tolist(), src[:E].tolist(),
-                        dst[:E].tolist(), w, prep.value)
+    bg = BlockedGraph(g.num_vertices, n, seg[:nseg.value].tolist(), src[:E].tolist(),
+                      dst[:E].tolist(), w, prep.value)
+    bg.graph = g
+    return bg
 
 
 blocked_for = block_edges
+
+
+def apply_blocked(bg, process_edge, runtime=None, make_context=None):
+    """Alg. 2 (blocking.py:116-186): ``process_edge`` once per edge of the
+    blocked layout, segments in order with a grid barrier between them, one
+    dispatch; returns the number of edges processed.
+
+    ``bg`` is the graph's blocked layout: a :class:`BlockedGraph` from
+    :func:`block_edges` (with ``bg.graph`` set) or a ``(graph, n)`` pair;
+    ``process_edge`` is a named device UDF (its atomic form runs per edge,
+    as the reference's EDGE_ONLY apply does).  ``make_context`` has no device
+    counterpart (per-worker Python contexts) and must be None.
+    """
+    from .engine import _device_udf
+    from .runtime import coerce_runtime
+    if make_context is not None:
+        raise EngineError("make_context callbacks cannot run on the device")
+    if isinstance(bg, tuple):
+        g, n = bg
+    else:
+        g, n = getattr(bg, "graph", None), bg.vertices_per_segment
+        if g is None:
+            raise EngineError("apply_blocked needs the device graph the layout was built "
+                              "from (block_edges(g, n) or (g, n))")
+    udf = _device_udf(process_edge)
+    rt = coerce_runtime(runtime, g)
+    st = udf.state()
+    edges = C.c_int64()
+    _lib.call("gg_apply_blocked", rt.handle, int(n), udf.code, C.byref(st), C.byref(edges))
+    return edges.value
 
 
 def save_blocked(bg, path):

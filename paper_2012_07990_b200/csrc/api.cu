@@ -63,6 +63,7 @@ struct gg_frontier {
   bool retired = false;
 };
 struct gg_blocked { Blocked* b; };
+struct gg_bucket_queue { BucketQueueDev* q; };
 
 #define GG_API_BEGIN try {
 #define GG_API_END                                                      \
@@ -477,6 +478,148 @@ int gg_edgeset_apply(gg_runtime* rt, int32_t udf, const gg_udf_state* state, int
       *out = nullptr;
     }
   }
+  GG_API_END
+}
+
+int gg_runtime_fused_region(gg_runtime* rt, int32_t enter) {
+  GG_API_BEGIN
+  NEED(rt);
+  Runtime& r = *rt->rt;
+  if (enter) {
+    r.stats.dispatch_count += 1;  // the whole region is one dispatch (runtime.py:194-196)
+    r.fused_depth += 1;
+  } else {
+    if (r.fused_depth <= 0) fail(GG_ERR_ENGINE, "no fused region to leave");
+    r.fused_depth -= 1;
+  }
+  GG_API_END
+}
+
+int gg_runtime_add_rounds(gg_runtime* rt, int64_t n) {
+  GG_API_BEGIN
+  NEED(rt);
+  rt->rt->stats.rounds += n;
+  GG_API_END
+}
+
+// ---- BucketQueue -------------------------------------------------------------
+static BucketQueueDev* bq(gg_bucket_queue* q) {
+  if (!q || !q->q) fail(GG_ERR_VALUE, "null bucket queue");
+  return q->q;
+}
+
+int gg_bucket_queue_create(int32_t device, int64_t universe, uint64_t delta, gg_bucket_queue** out) {
+  GG_API_BEGIN
+  NEED(out);
+  auto h = new gg_bucket_queue{nullptr};
+  try {
+    h->q = bq_create(device, universe, delta);
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  *out = h;
+  GG_API_END
+}
+
+int gg_bucket_queue_destroy(gg_bucket_queue* q) {
+  GG_API_BEGIN
+  if (q) {
+    bq_destroy(q->q);
+    delete q;
+  }
+  GG_API_END
+}
+
+int gg_bucket_queue_seed(gg_bucket_queue* q, int64_t v, uint64_t priority) {
+  GG_API_BEGIN
+  bq_seed(bq(q), v, priority);
+  GG_API_END
+}
+
+int gg_bucket_queue_update_min(gg_bucket_queue* q, int64_t v, uint64_t candidate, int32_t* improved) {
+  GG_API_BEGIN
+  bool r = bq_update_min(bq(q), v, candidate);
+  if (improved) *improved = r ? 1 : 0;
+  GG_API_END
+}
+
+int gg_bucket_queue_take_current(gg_bucket_queue* q, gg_frontier** taken) {
+  GG_API_BEGIN
+  NEED(taken);
+  auto h = new gg_frontier;
+  try {
+    h->f = bq_take_current(bq(q));
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  *taken = h;
+  GG_API_END
+}
+
+int gg_bucket_queue_recycle(gg_bucket_queue* q, gg_frontier* taken) {
+  GG_API_BEGIN
+  live(taken);
+  bq_recycle(bq(q), std::move(taken->f));
+  taken->retired = true;
+  GG_API_END
+}
+
+int gg_bucket_queue_advance(gg_bucket_queue* q, int32_t* nonempty) {
+  GG_API_BEGIN
+  bool r = bq_advance(bq(q));
+  if (nonempty) *nonempty = r ? 1 : 0;
+  GG_API_END
+}
+
+int gg_bucket_queue_info(gg_bucket_queue* q, uint64_t* index, int64_t* current_size, int64_t* far_size) {
+  GG_API_BEGIN
+  bq_info(bq(q), index, current_size, far_size);
+  GG_API_END
+}
+
+int gg_bucket_queue_members(gg_bucket_queue* q, int32_t which, int32_t* out, int64_t cap, int64_t* n) {
+  GG_API_BEGIN
+  NEED(n);
+  Frontier* f = bq_queue(bq(q), which ? 1 : 0);
+  DeviceGuard guard(f->dev);
+  const int64_t sz = frontier_size_raw(f, 0);
+  *n = sz;
+  if (sz > cap) fail(GG_ERR_VALUE, "output buffer too small");
+  if (sz) NEED(out);
+  frontier_members(f, out, sz, 0);
+  GG_API_END
+}
+
+int gg_bucket_queue_priorities(gg_bucket_queue* q, uint64_t* out) {
+  GG_API_BEGIN
+  BucketQueueDev* d = bq(q);
+  if (bq_universe(d)) NEED(out);
+  bq_copy_priorities(d, out);
+  GG_API_END
+}
+
+// ---- EdgeBlocking apply (blocking.py:116-186) ------------------------------------
+int gg_apply_blocked(gg_runtime* rt, int64_t n, int32_t udf, const gg_udf_state* state, int64_t* edges) {
+  GG_API_BEGIN
+  NEED(rt);
+  if (n < 1) fail(GG_ERR_VALUE, "vertices per segment must be >= 1");
+  gg_binding b{};
+  b.s1.direction = GG_PUSH;
+  b.s1.pull_repr = GG_BITMAP;
+  b.s1.load_balance = GG_LB_EDGE_ONLY;
+  b.s1.blocking = 1;
+  b.s1.blocking_size = n;
+  b.s1.frontier_creation = GG_CREATE_FUSED;
+  b.s1.delta = 1;
+  b.s2 = b.s1;
+  gg_udf_state st{};
+  if (state) st = *state;
+  DeviceGuard guard(rt->rt->dev);
+  const int64_t before = rt->rt->stats.edges_traversed;
+  edgeset_apply(rt->rt.get(), udf, st, false, nullptr, b, false, false);
+  if (edges) *edges = rt->rt->stats.edges_traversed - before;
   GG_API_END
 }
 

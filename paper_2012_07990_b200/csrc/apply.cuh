@@ -18,6 +18,21 @@ void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small
                int64_t entries = 0);
 OutBuilder make_builder(Runtime* rt, const gg_schedule& s, Frontier* out);
 void dense_size_on_device(Frontier* f, cudaStream_t s);
+// Named UDFs of the algorithm drivers, routed through gg_edgeset_apply
+// (each defined beside its driver so the apply_op instantiations are shared).
+std::unique_ptr<Frontier> apply_cc_hook(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                        std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                        bool reuse, bool collect);
+std::unique_ptr<Frontier> apply_bc_forward(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                           std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                           bool reuse, bool collect);
+std::unique_ptr<Frontier> apply_bc_backward(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                            std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                            bool reuse, bool collect);
+std::unique_ptr<Frontier> apply_sssp_relax(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                           std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                           bool reuse, bool collect);
+
 // sum of the out-degrees of the n entries of a SPARSE input (one round trip)
 int64_t degree_sum(Runtime* rt, const InView& in, int64_t n);
 

@@ -55,6 +55,26 @@ static int64_t snapshot(Runtime& rt, Frontier* f, int32_t* order, int64_t pos, D
   return cnt;
 }
 
+// gg_edgeset_apply(GG_UDF_BC_FORWARD): a forward round (algos.py:353-365);
+// state arr0 = int32 depth[V], arr1 = double sigma[V], i0 = level.
+std::unique_ptr<Frontier> apply_bc_forward(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                           std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                           bool reuse, bool collect) {
+  if (!st.arr0 || !st.arr1) fail(GG_ERR_VALUE, "bc forward needs depth and sigma arrays");
+  return apply_op(rt, OpBcFwd{(int32_t*)st.arr0, (double*)st.arr1, (int32_t)st.i0}, use_filter, in,
+                  b, reuse, collect);
+}
+
+// gg_edgeset_apply(GG_UDF_BC_BACKWARD): a backward round (algos.py:378-382),
+// push only; state arr0 = depth, arr1 = sigma, arr2 = double delta[V].
+std::unique_ptr<Frontier> apply_bc_backward(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                            std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                            bool reuse, bool collect) {
+  if (!st.arr0 || !st.arr1 || !st.arr2) fail(GG_ERR_VALUE, "bc backward needs depth, sigma and delta");
+  return apply_op(rt, OpBcBwd{(const int32_t*)st.arr0, (const double*)st.arr1, (double*)st.arr2},
+                  use_filter, in, b, reuse, collect);
+}
+
 void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_binding& b, Runtime& rt,
             double* scores_out) {
   if (nsrc <= 0) fail(GG_ERR_VALUE, "sources must be a non-empty list");

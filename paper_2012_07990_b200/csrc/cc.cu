@@ -47,6 +47,15 @@ __global__ void k_cc_canon(const int32_t* label, const int32_t* first, int64_t V
     out[v] = first[label[v]];
 }
 
+// gg_edgeset_apply(GG_UDF_CC_HOOK): one hooking apply of cc_soman's body
+// (algos.py:283-297); state arr0 = int32 label[V], arr1 = int changed flag.
+std::unique_ptr<Frontier> apply_cc_hook(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                        std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                        bool reuse, bool collect) {
+  if (!st.arr0 || !st.arr1) fail(GG_ERR_VALUE, "cc hook needs label and changed-flag arrays");
+  return apply_op(rt, OpHook{(int32_t*)st.arr0, (int*)st.arr1}, use_filter, in, b, reuse, collect);
+}
+
 void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32_t* labels_out) {
   if (b.is_hybrid)
     fail(GG_ERR_SCHEDULE, "label 's0:s1' of cc takes a SimpleGPUSchedule (hybrid direction "

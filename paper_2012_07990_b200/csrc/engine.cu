@@ -802,6 +802,14 @@ std::unique_ptr<Frontier> edgeset_apply(Runtime* rt, int udf, const gg_udf_state
     case UDF_PR32:
       return apply_op(rt, OpPr<float>{(double*)st.arr0, (const float*)st.arr1}, use_filter, input, b,
                       reuse, collect_output);
+    case UDF_CC_HOOK:
+      return apply_cc_hook(rt, st, use_filter, input, b, reuse, collect_output);
+    case UDF_BC_FORWARD:
+      return apply_bc_forward(rt, st, use_filter, input, b, reuse, collect_output);
+    case UDF_BC_BACKWARD:
+      return apply_bc_backward(rt, st, use_filter, input, b, reuse, collect_output);
+    case UDF_SSSP_RELAX:
+      return apply_sssp_relax(rt, st, use_filter, input, b, reuse, collect_output);
     default:
       fail(GG_ERR_VALUE, "unknown udf id");
   }

@@ -101,11 +101,27 @@ void check_schedule(const gg_schedule& s);
 void check_binding(const gg_binding& b);
 
 enum UdfKind { UDF_BFS = GG_UDF_BFS, UDF_COUNT = GG_UDF_COUNT, UDF_ENQUEUE = GG_UDF_ENQUEUE,
-               UDF_PR = GG_UDF_PR, UDF_PR32 = 100 };
+               UDF_PR = GG_UDF_PR, UDF_CC_HOOK = GG_UDF_CC_HOOK, UDF_BC_FORWARD = GG_UDF_BC_FORWARD,
+               UDF_BC_BACKWARD = GG_UDF_BC_BACKWARD, UDF_SSSP_RELAX = GG_UDF_SSSP_RELAX,
+               UDF_PR32 = 100 };
 
 // One edgeset.apply round with a named UDF; returns the output frontier
 // (null when collect_output is false).  `input` may be null (all active).
 // When reuse is set, the input is released to the pool.
+// Device BucketQueue (priority.py:17-118), sssp.cu
+struct BucketQueueDev;
+BucketQueueDev* bq_create(int dev, int64_t universe, uint64_t delta);
+void bq_destroy(BucketQueueDev* q);
+void bq_seed(BucketQueueDev* q, int64_t v, uint64_t priority);
+std::unique_ptr<Frontier> bq_take_current(BucketQueueDev* q);
+void bq_recycle(BucketQueueDev* q, std::unique_ptr<Frontier> taken);
+bool bq_update_min(BucketQueueDev* q, int64_t v, uint64_t candidate);
+bool bq_advance(BucketQueueDev* q);
+void bq_info(BucketQueueDev* q, uint64_t* index, int64_t* ncur, int64_t* nfar);
+void bq_copy_priorities(BucketQueueDev* q, uint64_t* dst);
+Frontier* bq_queue(BucketQueueDev* q, int which);  // 0 current, 1 far
+int64_t bq_universe(const BucketQueueDev* q);
+
 std::unique_ptr<Frontier> edgeset_apply(Runtime* rt, int udf, const gg_udf_state& st, bool use_filter,
                                         std::unique_ptr<Frontier>* input, const gg_binding& b,
                                         bool reuse, bool collect_output);

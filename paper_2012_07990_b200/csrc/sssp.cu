@@ -205,6 +205,187 @@ __global__ void __launch_bounds__(256) k_sssp_fused(SsspFusedArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// BucketQueue as a device object (priority.py:17-118) for custom loops:
+// priorities u64[V] (UNREACHED = 2^64-1), current / far SPARSE queues with
+// byte-mark dedup (per round for current, until advance for far), a spare
+// for recycle().  Host calls order on the legacy stream like every driver.
+// ---------------------------------------------------------------------------
+struct BucketQueueDev {
+  int dev = 0;
+  int64_t V = 0;
+  unsigned long long delta = 1;
+  unsigned long long index = 0;
+  DevBuf<unsigned long long> prio, best;
+  DevBuf<uint8_t> cmark, fmark;
+  DevBuf<int> flag;
+  std::unique_ptr<Frontier> cur, far, far2, spare;
+};
+
+__global__ void k_bq_update(unsigned long long* prio, int64_t v, unsigned long long cand,
+                            unsigned long long delta, unsigned long long index, OutBuilder cur,
+                            OutBuilder far, int* improved, int seed) {
+  if (seed) {  // seed(): the priority is set, the vertex enters current (priority.py:35-39)
+    prio[v] = cand;
+    cur.emit((int32_t)v);
+    *improved = 1;
+    return;
+  }
+  unsigned long long old = atomicMin(prio + v, cand);
+  *improved = cand < old;
+  if (cand < old) {
+    if (cand / delta == index) cur.emit((int32_t)v);
+    else far.emit((int32_t)v);
+  }
+}
+
+BucketQueueDev* bq_create(int dev, int64_t V, uint64_t delta) {
+  if (delta < 1) fail(GG_ERR_VALUE, "delta must be >= 1");
+  if (V < 0) fail(GG_ERR_VALUE, "universe must be >= 0");
+  DeviceGuard guard(dev);
+  auto q = std::make_unique<BucketQueueDev>();
+  q->dev = dev;
+  q->V = V;
+  q->delta = delta;
+  q->prio.alloc(V);
+  GG_CUDA(cudaMemsetAsync(q->prio.p, 0xff, std::max<int64_t>(V, 1) * 8, 0));
+  const int64_t mb = ((V + 3) & ~int64_t(3)) + 4;
+  q->cmark.alloc(mb);
+  q->fmark.alloc(mb);
+  q->cmark.zero();
+  q->fmark.zero();
+  q->best.alloc(1);
+  q->flag.alloc(1);
+  q->cur = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+  q->far = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+  q->far2 = frontier_alloc(dev, V, GG_SPARSE, V + 1);
+  return q.release();
+}
+
+void bq_destroy(BucketQueueDev* q) {
+  if (!q) return;
+  DeviceGuard guard(q->dev);
+  GG_CUDA(cudaStreamSynchronize(0));
+  delete q;
+}
+
+static void bq_check_vertex(const BucketQueueDev* q, int64_t v) {
+  if (v < 0 || v >= q->V)
+    fail(GG_ERR_VALUE, strf("vertex %lld out of range [0, %lld)", (long long)v, (long long)q->V));
+}
+
+static bool bq_point_update(BucketQueueDev* q, int64_t v, uint64_t cand, int seed) {
+  DeviceGuard guard(q->dev);
+  k_bq_update<<<1, 1>>>(q->prio.p, v, cand, q->delta, q->index, queue_builder(q->cur.get(), q->cmark.p),
+                        queue_builder(q->far.get(), q->fmark.p), q->flag.p, seed);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  q->cur->size_cache = -1;
+  q->far->size_cache = -1;
+  int h = 0;
+  GG_CUDA(cudaMemcpy(&h, q->flag.p, sizeof(int), cudaMemcpyDeviceToHost));
+  return h != 0;
+}
+
+void bq_seed(BucketQueueDev* q, int64_t v, uint64_t priority) {
+  bq_check_vertex(q, v);
+  q->index = priority / q->delta;  // the bucket index snaps to the seed's bucket
+  bq_point_update(q, v, priority, 1);
+}
+
+bool bq_update_min(BucketQueueDev* q, int64_t v, uint64_t candidate) {
+  bq_check_vertex(q, v);
+  return bq_point_update(q, v, candidate, 0);
+}
+
+std::unique_ptr<Frontier> bq_take_current(BucketQueueDev* q) {
+  DeviceGuard guard(q->dev);
+  std::unique_ptr<Frontier> taken = std::move(q->cur);
+  // clear the per-round marks of the taken ids (priority.py:47)
+  k_clear_byte_marks<<<grid_for(std::max<int64_t>(q->V, 1), 256, q->dev), 256>>>(
+      taken->ids.p, taken->count.p, q->cmark.p);
+  GG_LAUNCH_CHECK();
+  count_launch();
+  if (q->spare) {
+    q->cur = std::move(q->spare);
+    q->cur->retired = false;
+  } else {
+    q->cur = frontier_alloc(q->dev, q->V, GG_SPARSE, q->V + 1);
+  }
+  frontier_clear(q->cur.get(), 0);
+  taken->size_cache = -1;
+  return taken;
+}
+
+void bq_recycle(BucketQueueDev* q, std::unique_ptr<Frontier> taken) {
+  if (!taken) return;
+  if (taken->universe != q->V || taken->repr != GG_SPARSE || (int64_t)taken->ids.n < q->V + 1)
+    fail(GG_ERR_FRONTIER, "recycle takes a bucket handed out by take_current");
+  frontier_clear(taken.get(), 0);
+  if (!q->spare) q->spare = std::move(taken);
+}
+
+bool bq_advance(BucketQueueDev* q) {
+  DeviceGuard guard(q->dev);
+  if (frontier_size_raw(q->cur.get(), 0) != 0)
+    fail(GG_ERR_ENGINE, "advance with a non-empty current bucket");
+  const unsigned grid = (unsigned)sm_count(q->dev) * 8;
+  GG_CUDA(cudaMemsetAsync(q->best.p, 0xff, 8, 0));
+  k_adv_min<<<grid, 256>>>(q->far->ids.p, q->far->count.p, q->prio.p, q->delta, q->index, q->fmark.p,
+                           q->best.p);
+  GG_LAUNCH_CHECK();
+  unsigned long long hb = 0;
+  GG_CUDA(cudaMemcpy(&hb, q->best.p, 8, cudaMemcpyDeviceToHost));
+  frontier_clear(q->far2.get(), 0);
+  if (hb != kUnreached) {
+    k_adv_split<<<grid, 256>>>(q->far->ids.p, q->far->count.p, q->prio.p, q->delta, q->index, q->best.p,
+                               queue_builder(q->cur.get(), q->cmark.p),
+                               queue_builder(q->far2.get(), q->fmark.p));
+    GG_LAUNCH_CHECK();
+    q->index = hb;
+  }
+  count_launch(hb != kUnreached ? 2 : 1);
+  frontier_clear(q->far.get(), 0);
+  std::swap(q->far, q->far2);
+  q->cur->size_cache = -1;
+  q->far->size_cache = -1;
+  return hb != kUnreached;
+}
+
+void bq_info(BucketQueueDev* q, uint64_t* index, int64_t* ncur, int64_t* nfar) {
+  DeviceGuard guard(q->dev);
+  if (index) *index = q->index;
+  if (ncur) *ncur = frontier_size_raw(q->cur.get(), 0);
+  if (nfar) *nfar = frontier_size_raw(q->far.get(), 0);
+}
+
+void bq_copy_priorities(BucketQueueDev* q, uint64_t* dst) {
+  DeviceGuard guard(q->dev);
+  if (q->V) GG_CUDA(cudaMemcpy(dst, q->prio.p, q->V * 8, cudaMemcpyDefault));
+}
+
+Frontier* bq_queue(BucketQueueDev* q, int which) { return which ? q->far.get() : q->cur.get(); }
+int64_t bq_universe(const BucketQueueDev* q) { return q->V; }
+
+// gg_edgeset_apply(GG_UDF_SSSP_RELAX): update_priority_min(dst, prio[src] + w)
+// for every arc of the input (algos.py:233-234); state arr0 = the queue.
+std::unique_ptr<Frontier> apply_sssp_relax(Runtime* rt, const gg_udf_state& st, bool use_filter,
+                                           std::unique_ptr<Frontier>* in, const gg_binding& b,
+                                           bool reuse, bool collect) {
+  auto* q = static_cast<BucketQueueDev*>(st.arr0);
+  if (!q) fail(GG_ERR_VALUE, "sssp relax needs a bucket queue");
+  if (q->V != rt->g->V)
+    fail(GG_ERR_ENGINE, strf("bucket queue universe %lld does not match graph (%lld vertices)",
+                             (long long)q->V, (long long)rt->g->V));
+  if (!rt->g->weighted) fail(GG_ERR_VALUE, "sssp relax needs edge weights");
+  OpRelax op{q->prio.p, q->delta, q->index, queue_builder(q->cur.get(), q->cmark.p),
+             queue_builder(q->far.get(), q->fmark.p)};
+  auto out = apply_op(rt, op, use_filter, in, b, reuse, collect);
+  q->cur->size_cache = -1;
+  q->far->size_cache = -1;
+  return out;
+}
+
 void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
               uint64_t* dist_out) {
   if (source < 0 || source >= g.V)

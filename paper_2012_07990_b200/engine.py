@@ -236,18 +236,31 @@ def hybrid_apply(g, input_frontier, udf_push, udf_pull, hybrid, *, to_filter=Non
 
 
 def fused_loop(body, until, *, fusion=False, runtime=None, body_reuses_frontiers=True):
-    """Host loop driver with the reference's accounting (engine.py:639-662).
+    """Run ``body`` until ``until()`` (engine.py:639-662).
 
-    The algorithm drivers in ``algos`` fuse on the device (one cooperative
-    launch); this host-level helper keeps the reference contract for custom
-    loops: fusion requires a frontier-reusing body.
+    Unfused, each traversal in the body is its own dispatch; fused, the
+    whole loop is ONE dispatch (Runtime.fused_dispatch, runtime.py:194-209)
+    and the body must recycle frontier storage.  The algorithm drivers in
+    ``algos`` fuse on the device as one cooperative launch; a custom host
+    body keeps its per-round launches but is accounted as one dispatch,
+    exactly as the reference's fused region is one pool dispatch.  With a
+    bound :class:`Runtime` the rounds land in its device stats.
     """
     if fusion and not body_reuses_frontiers:
         raise ScheduleError("kernel fusion requires a loop body that reuses frontier storage")
+    rt = runtime if isinstance(runtime, Runtime) and runtime._handle is not None else None
     rounds = 0
-    while not until():
-        body()
-        rounds += 1
-    st = runtime.stats if isinstance(runtime, Runtime) else RunStats()
-    st.rounds = max(st.rounds, rounds)
+    if fusion and rt is not None:
+        _lib.call("gg_runtime_fused_region", rt.handle, 1)
+    try:
+        while not until():
+            body()
+            rounds += 1
+    finally:
+        if fusion and rt is not None:
+            _lib.call("gg_runtime_fused_region", rt.handle, 0)
+    if rt is not None:
+        _lib.call("gg_runtime_add_rounds", rt.handle, rounds)
+        return rt.stats
+    st = RunStats(rounds=rounds, dispatch_count=1 if fusion else 0)
     return st

@@ -28,10 +28,8 @@ class DeviceUDF:
 
     def state(self):
         st = _lib.GGUdfState()
-        if len(self.arrays) > 0:
-            st.arr0 = self.arrays[0].data_ptr()
-        if len(self.arrays) > 1:
-            st.arr1 = self.arrays[1].data_ptr()
+        for k, a in enumerate(self.arrays[:3]):
+            setattr(st, "arr%d" % k, a.data_ptr())
         return st
 
 
@@ -54,3 +52,56 @@ class EnqueueDst(DeviceUDF):
 class PageRankGather(DeviceUDF):
     """atomic_add(acc[dst], contrib[src]) (algos.py:180-181); f64 tensors."""
     code = _lib.UDF_PR
+
+
+class CcHook(DeviceUDF):
+    """cc_soman's hook (algos.py:283-293): la, lb = label[src], label[dst];
+    atomic_min(label, max(la, lb), min(la, lb)); a lowering sets changed[0].
+    label: int32 CUDA tensor (V); changed: int32 CUDA tensor (1)."""
+    code = _lib.UDF_CC_HOOK
+
+    def __init__(self, label, changed):
+        super().__init__(label, changed)
+
+
+class BcForward(DeviceUDF):
+    """bc's forward round at ``level`` (algos.py:353-365): CAS depth[dst]
+    -1 -> level+1 with enqueue, sigma[dst] += sigma[src] when depth[dst] ==
+    level+1; filter depth == -1 or level+1 (push) / owner store (pull).
+    depth: int32, sigma: float64 CUDA tensors (V)."""
+    code = _lib.UDF_BC_FORWARD
+
+    def __init__(self, depth, sigma, level=0):
+        super().__init__(depth, sigma)
+        self.level = level
+
+    def state(self):
+        st = super().state()
+        st.i0 = int(self.level)
+        return st
+
+
+class BcBackward(DeviceUDF):
+    """bc's backward round (algos.py:378-382), push only: delta[src] +=
+    sigma[src]/sigma[dst]*(1+delta[dst]) when depth[dst] == depth[src]+1.
+    depth: int32, sigma / delta: float64 CUDA tensors (V)."""
+    code = _lib.UDF_BC_BACKWARD
+
+    def __init__(self, depth, sigma, delta):
+        super().__init__(depth, sigma, delta)
+
+
+class SsspRelax(DeviceUDF):
+    """sssp_delta's relaxation (algos.py:233-234):
+    queue.update_priority_min(dst, priorities[src] + weight) on a device
+    :class:`~paper_2012_07990_b200.priority.BucketQueue`."""
+    code = _lib.UDF_SSSP_RELAX
+
+    def __init__(self, queue):
+        super().__init__()
+        self.queue = queue
+
+    def state(self):
+        st = _lib.GGUdfState()
+        st.arr0 = self.queue.handle
+        return st

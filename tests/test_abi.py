@@ -36,3 +36,35 @@ def test_library_reports_errors_without_a_device():
     assert lib.gg_device_count(C.byref(n)) == 0
     assert n.value >= 0
     assert lib.gg_version().startswith(b"gg-b200")
+
+
+# the reference package's export list (schedge/__init__.py:26-38)
+REFERENCE_ALL = [
+    "ALGO_LABELS", "ALGO_NAMES", "AlgoResult", "bc", "bfs", "bfs_levels", "cc_soman",
+    "pagerank", "sssp_delta", "BlockedGraph", "apply_blocked", "block_edges", "BITMAP",
+    "BOOLMAP", "SPARSE", "VertexSubset", "Graph", "GraphLoadError", "load_edge_list",
+    "load_graph", "load_matrix_market", "out_degree", "with_random_weights", "UNREACHED",
+    "BucketQueue", "EdgeContext", "EngineError", "ExecConfig", "RunStats", "Runtime",
+    "HybridSchedule", "ParseError", "Schedule", "ScheduleError", "ScheduleProgram",
+    "enumerate_space", "parse_schedule", "pretty_print", "validate", "edgeset_apply",
+    "fused_loop", "hybrid_apply", "__version__",
+]
+
+
+def test_package_exports_the_reference_surface():
+    import paper_2012_07990_b200 as gg
+    assert [n for n in REFERENCE_ALL if not hasattr(gg, n)] == []
+    assert set(REFERENCE_ALL) <= set(gg.__all__)
+
+
+def test_every_algorithm_udf_has_a_device_id():
+    from paper_2012_07990_b200 import _lib, udfs
+    codes = {c.code for c in (udfs.BfsParent, udfs.CountInDegree, udfs.EnqueueDst,
+                              udfs.PageRankGather, udfs.CcHook, udfs.BcForward,
+                              udfs.BcBackward, udfs.SsspRelax)}
+    assert codes == set(range(8))
+    text = open(os.path.join(ROOT, "include", "gg.h")).read()
+    for name in ("GG_UDF_CC_HOOK = 4", "GG_UDF_BC_FORWARD = 5", "GG_UDF_BC_BACKWARD = 6",
+                 "GG_UDF_SSSP_RELAX = 7"):
+        assert name in text
+    assert _lib.UDF_SSSP_RELAX == 7
