@@ -65,6 +65,11 @@ struct gg_frontier {
 struct gg_blocked { Blocked* b; };
 struct gg_bucket_queue { BucketQueueDev* q; };
 
+static BucketQueueDev* bq(gg_bucket_queue* q) {
+  if (!q || !q->q) fail(GG_ERR_VALUE, "null bucket queue");
+  return q->q;
+}
+
 #define GG_API_BEGIN try {
 #define GG_API_END                                                      \
   return GG_OK;                                                         \
@@ -465,6 +470,7 @@ int gg_edgeset_apply(gg_runtime* rt, int32_t udf, const gg_udf_state* state, int
   if (input) live(input);
   gg_udf_state st{};
   if (state) st = *state;
+  if (udf == GG_UDF_SSSP_RELAX) st.arr0 = bq(static_cast<gg_bucket_queue*>(st.arr0));  // handle -> queue
   DeviceGuard guard(rt->rt->dev);
   auto res = edgeset_apply(rt->rt.get(), udf, st, filter != 0, input ? &input->f : nullptr, *binding,
                            reuse != 0, collect_output != 0);
@@ -503,10 +509,6 @@ int gg_runtime_add_rounds(gg_runtime* rt, int64_t n) {
 }
 
 // ---- BucketQueue -------------------------------------------------------------
-static BucketQueueDev* bq(gg_bucket_queue* q) {
-  if (!q || !q->q) fail(GG_ERR_VALUE, "null bucket queue");
-  return q->q;
-}
 
 int gg_bucket_queue_create(int32_t device, int64_t universe, uint64_t delta, gg_bucket_queue** out) {
   GG_API_BEGIN
@@ -618,6 +620,7 @@ int gg_apply_blocked(gg_runtime* rt, int64_t n, int32_t udf, const gg_udf_state*
   if (state) st = *state;
   DeviceGuard guard(rt->rt->dev);
   const int64_t before = rt->rt->stats.edges_traversed;
+  if (udf == GG_UDF_SSSP_RELAX) st.arr0 = bq(static_cast<gg_bucket_queue*>(st.arr0));
   edgeset_apply(rt->rt.get(), udf, st, false, nullptr, b, false, false);
   if (edges) *edges = rt->rt->stats.edges_traversed - before;
   GG_API_END
