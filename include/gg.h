@@ -236,6 +236,14 @@ int gg_edgeset_apply(gg_runtime* rt, int32_t udf, const gg_udf_state* state, int
                      gg_frontier* input /* NULL = all vertices */, const gg_binding* binding,
                      int32_t reuse, int32_t collect_output, gg_frontier** out);
 
+/* The device balancers' split of a SPARSE active list, for pinning against
+ * the reference partitioners (engine.py:51-142): ETWC -> 3 values per entry
+ * (stage 0 / 1 / 2 edge counts, engine.py:62-85), TWC -> the bin per entry
+ * (0 thread, 1 warp, 2 CTA; engine.py:131-142), STRICT -> the exclusive
+ * degree prefix, n + 1 values (engine.py:116-122).  *n = values written. */
+int gg_partition_dump(gg_runtime* rt, gg_frontier* active, int32_t load_balance, int64_t* out,
+                      int64_t cap, int64_t* n);
+
 /* engine.fused_loop / Runtime.fused_dispatch (engine.py:639-662,
  * runtime.py:194-209): enter = 1 opens a fused region (one dispatch for
  * everything inside, counted now), enter = 0 closes it; add_rounds adds loop

@@ -187,6 +187,20 @@ def c1_pagerank():
     return {"build_s": build, "run_s": run, "sha": h}
 
 
+def sidecars():
+    """Blocked-graph sidecars written by the reference's own save_blocked
+    (blocking.py:189-217): a weighted RMAT-8 at two widths."""
+    V, s, d = gen.rmat(8, 4, seed=11)
+    w = gen.weights(len(s), 11)
+    g = Graph.from_coo(V, s.tolist(), d.tolist(), w.astype(np.int64).tolist())
+    for n in (16, 100):
+        bg = blocking.block_edges(g, n)
+        blocking.save_blocked(bg, os.path.join(OUT, "ref_sidecar_rmat8_n%d.blk" % n))
+    gu = Graph.from_coo(V, s.tolist(), d.tolist())
+    blocking.save_blocked(blocking.block_edges(gu, 32),
+                          os.path.join(OUT, "ref_sidecar_rmat8_unweighted_n32.blk"))
+
+
 def rmat12_cases():
     """Scale-12 RMAT (symmetrised for BFS/CC/BC, weighted for SSSP)."""
     V, s, d = gen.rmat(12, 16, seed=2)
@@ -267,3 +281,4 @@ if __name__ == "__main__":
     print("c1:", c1_pagerank())
     tune_candidates()
     scale16_cases()
+    sidecars()

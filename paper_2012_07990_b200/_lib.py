@@ -108,6 +108,7 @@ SIGNATURES = {
     "gg_frontier_convert": (I32, [VP, VP, I32, PP]),
     "gg_edgeset_apply": (I32, [VP, I32, C.POINTER(GGUdfState), I32, VP,
                                C.POINTER(GGBinding), I32, I32, PP]),
+    "gg_partition_dump": (I32, [VP, VP, I32, VP, I64, C.POINTER(I64)]),
     "gg_runtime_fused_region": (I32, [VP, I32]),
     "gg_runtime_add_rounds": (I32, [VP, I64]),
     "gg_bucket_queue_create": (I32, [I32, I64, U64, PP]),

@@ -508,6 +508,17 @@ int gg_runtime_add_rounds(gg_runtime* rt, int64_t n) {
   GG_API_END
 }
 
+int gg_partition_dump(gg_runtime* rt, gg_frontier* active, int32_t load_balance, int64_t* out,
+                      int64_t cap, int64_t* n) {
+  GG_API_BEGIN
+  NEED(rt);
+  NEED(n);
+  Frontier* f = live(active);
+  DeviceGuard guard(rt->rt->dev);
+  *n = partition_dump(rt->rt.get(), f, load_balance, out, cap);
+  GG_API_END
+}
+
 // ---- BucketQueue -------------------------------------------------------------
 
 int gg_bucket_queue_create(int32_t device, int64_t universe, uint64_t delta, gg_bucket_queue** out) {

@@ -698,6 +698,51 @@ int64_t degree_sum(Runtime* rt, const InView& in, int64_t n) {
   return (int64_t)h;
 }
 
+__global__ void k_split_dump(const InView in, const int64_t* off, int64_t n, int lb, int cta,
+                             int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = active_at(in, i);
+    const int64_t size = off[u + 1] - off[u];
+    if (lb == GG_LB_ETWC) {
+      const EtwcSizes s = etwc_sizes(size, cta);
+      out[3 * i] = s.e0;
+      out[3 * i + 1] = s.e1;
+      out[3 * i + 2] = s.e2;
+    } else {
+      out[i] = twc_bin_of(size, cta);
+    }
+  }
+}
+
+void strict_prefix(Runtime* rt, const InView& in, int64_t n);
+
+int64_t partition_dump(Runtime* rt, Frontier* active, int lb, int64_t* out, int64_t cap) {
+  if (active->repr != GG_SPARSE) fail(GG_ERR_FRONTIER, "partition dump takes a SPARSE active list");
+  rt->g->ensure_out();
+  const int64_t n = frontier_size_raw(active, rt->stream);
+  const InView in = active->view();
+  int64_t len = 0;
+  if (lb == GG_LB_STRICT) {
+    len = n + 1;
+    if (len > cap) fail(GG_ERR_VALUE, "output buffer too small");
+    strict_prefix(rt, in, n);
+    GG_CUDA(cudaMemcpy(out, rt->prefix.p, len * 8, cudaMemcpyDefault));
+    return len;
+  }
+  if (lb != GG_LB_ETWC && lb != GG_LB_TWC) fail(GG_ERR_VALUE, "partition dump covers ETWC, TWC, STRICT");
+  len = lb == GG_LB_ETWC ? 3 * n : n;
+  if (len > cap) fail(GG_ERR_VALUE, "output buffer too small");
+  if (!n) return 0;
+  DevBuf<int64_t> d(len);
+  k_split_dump<<<grid_for(n, 256, rt->dev), 256, 0, rt->stream>>>(in, rt->g->out_view().off, n, lb,
+                                                                  rt->cfg.cta_size, d.p);
+  GG_LAUNCH_CHECK();
+  GG_CUDA(cudaMemcpyAsync(out, d.p, len * 8, cudaMemcpyDefault, rt->stream));
+  GG_CUDA(cudaStreamSynchronize(rt->stream));
+  return len;
+}
+
 void strict_prefix(Runtime* rt, const InView& in, int64_t n) {
   cudaStream_t st = rt->stream;
   rt->prefix.alloc(n + 1);

@@ -122,6 +122,11 @@ void bq_copy_priorities(BucketQueueDev* q, uint64_t* dst);
 Frontier* bq_queue(BucketQueueDev* q, int which);  // 0 current, 1 far
 int64_t bq_universe(const BucketQueueDev* q);
 
+// The device balancers' per-vertex split of an active list (test hook):
+// ETWC -> (e0, e1, e2) stage sizes per entry, TWC -> bin per entry, STRICT ->
+// the exclusive degree prefix (n + 1).  Returns the number of values.
+int64_t partition_dump(Runtime* rt, Frontier* active, int lb, int64_t* out, int64_t cap);
+
 std::unique_ptr<Frontier> edgeset_apply(Runtime* rt, int udf, const gg_udf_state& st, bool use_filter,
                                         std::unique_ptr<Frontier>* input, const gg_binding& b,
                                         bool reuse, bool collect_output);

@@ -22,6 +22,21 @@ namespace cg = cooperative_groups;
 
 constexpr int kWarp = 32;
 
+// ETWC split of one vertex's edge range (engine.py:62-85): a cta multiple
+// (stage 2), then a warp multiple (stage 1), then the remainder (stage 0).
+struct EtwcSizes {
+  int64_t e2, e1, e0;
+};
+__host__ __device__ __forceinline__ EtwcSizes etwc_sizes(int64_t size, int cta) {
+  const int64_t e2 = (size / cta) * cta;
+  const int64_t e1 = ((size - e2) / kWarp) * kWarp;
+  return {e2, e1, size - e2 - e1};
+}
+// TWC bin (engine.py:131-142): promotion is strictly greater.
+__host__ __device__ __forceinline__ int twc_bin_of(int64_t deg, int cta) {
+  return deg > cta ? 2 : (deg > kWarp ? 1 : 0);
+}
+
 // ---------------------------------------------------------------------------
 // Read-only views
 // ---------------------------------------------------------------------------
@@ -390,7 +405,7 @@ __device__ __forceinline__ void b_twc_bin(PushArgs<Op> a, TwcQueues q, int cta) 
       a.huge[atomicAdd(a.huge_n, 1ULL)] = EtwcEntry{lo, (int32_t)deg, u};
       continue;
     }
-    int b = deg > cta ? 2 : (deg > kWarp ? 1 : 0);
+    int b = twc_bin_of(deg, cta);
     cg::coalesced_group g = cg::coalesced_threads();
     cg::coalesced_group gb = cg::labeled_partition(g, b);
     unsigned long long base = 0;
@@ -644,9 +659,8 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
     }
     int64_t size = end - start;
     sc += size;
-    int64_t e2 = (size / cta) * cta;
-    int64_t e1 = ((size - e2) / kWarp) * kWarp;
-    int64_t e0 = size - e2 - e1;
+    const EtwcSizes sz = etwc_sizes(size, cta);
+    int64_t e2 = sz.e2, e1 = sz.e1, e0 = sz.e0;
     EtwcEntry c2{start, (int32_t)e2, u}, c1{start + e2, (int32_t)e1, u},
         c0{start + e2 + e1, (int32_t)e0, u};
     if (a.huge && e2 >= a.huge_min) {  // whole-grid pass after this kernel / phase
@@ -887,7 +901,7 @@ __device__ __forceinline__ void b_pull_twc_bin(PullArgs<Op> a, TwcQueues q, int 
     if (a.use_filter && !a.op.filter((int32_t)v)) continue;
     int64_t deg = __ldg(a.g.off + v + 1) - __ldg(a.g.off + v);
     sc += deg;
-    int b = deg > cta ? 2 : (deg > kWarp ? 1 : 0);
+    int b = twc_bin_of(deg, cta);
     cg::coalesced_group g = cg::coalesced_threads();
     cg::coalesced_group gb = cg::labeled_partition(g, b);
     unsigned long long base = 0;
@@ -986,9 +1000,8 @@ __device__ __forceinline__ void b_pull_etwc(PullArgs<Op> a, int cta) {
     }
     int64_t size = end - start;
     sc += size;
-    int64_t e2 = (size / cta) * cta;
-    int64_t e1 = ((size - e2) / kWarp) * kWarp;
-    int64_t e0 = size - e2 - e1;
+    const EtwcSizes sz = etwc_sizes(size, cta);
+    int64_t e2 = sz.e2, e1 = sz.e1, e0 = sz.e0;
     EtwcEntry c[3] = {{start + e2 + e1, (int32_t)e0, (int32_t)v}, {start + e2, (int32_t)e1, (int32_t)v},
                       {start, (int32_t)e2, (int32_t)v}};
     bool has[3] = {e0 > 0, e1 > 0, e2 > 0};

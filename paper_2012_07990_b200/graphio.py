@@ -178,122 +178,147 @@ def symmetrize_coo(src, dst, weights=None):
     return a[keep], b[keep], w2, int(2 * len(src) - len(keep))
 
 
-def load_edge_list(path, weighted=False, symmetrize=False, device=0):
-    """Whitespace edge list ("src dst [w]"), '#'/'%' comments (graphio.py:143-191)."""
-    src, dst, wts = [], [], [] if weighted else None
-    comments = 0
+def _records(path, skip_first=False):
+    """(line number, tokens) of every non-blank, non-comment line."""
     with open(path) as fh:
         for lineno, raw in enumerate(fh, 1):
-            line = raw.strip()
-            if not line:
+            if skip_first and lineno == 1:
                 continue
-            if line[0] in "#%":
-                comments += 1
-                continue
-            parts = line.split()
-            if len(parts) < 2:
-                raise GraphLoadError("%s:%d: malformed edge line %r" % (path, lineno, line))
-            try:
-                u, v = int(parts[0]), int(parts[1])
-            except ValueError:
-                raise GraphLoadError("%s:%d: non-integer vertex id in %r"
-                                     % (path, lineno, line)) from None
-            if u < 0 or v < 0:
-                raise GraphLoadError("%s:%d: negative vertex id" % (path, lineno))
-            if weighted:
-                if len(parts) < 3:
-                    raise GraphLoadError("%s:%d: missing weight token" % (path, lineno))
-                try:
-                    wt = int(parts[2])
-                except ValueError:
-                    raise GraphLoadError("%s:%d: non-integer weight %r"
-                                         % (path, lineno, parts[2])) from None
-                if wt < 0:
-                    raise GraphLoadError("%s:%d: negative weight" % (path, lineno))
-                wts.append(wt)
-            src.append(u)
-            dst.append(v)
-    if not src:
+            toks = raw.split()
+            if toks and toks[0][0] not in "#%":
+                yield lineno, toks
+
+
+def _count_comments(path):
+    with open(path) as fh:
+        return sum(1 for raw in fh if raw.strip()[:1] in ("#", "%"))
+
+
+def _as_int(tok, where, what):
+    try:
+        return int(tok)
+    except ValueError:
+        raise GraphLoadError("%s: non-integer %s %r" % (where, what, tok)) from None
+
+
+class _Columns:
+    """Growing src / dst / weight columns with the loaders' checks."""
+
+    def __init__(self, weighted):
+        self.src, self.dst = [], []
+        self.w = [] if weighted else None
+
+    def add(self, u, v, w=None):
+        self.src.append(u)
+        self.dst.append(v)
+        if self.w is not None:
+            self.w.append(w)
+
+    def arrays(self):
+        s = np.asarray(self.src, np.int64)
+        d = np.asarray(self.dst, np.int64)
+        return s, d, (None if self.w is None else np.asarray(self.w, np.int64))
+
+
+def load_edge_list(path, weighted=False, symmetrize=False, device=0):
+    """"src dst [weight]" per line, '#'/'%' comments (the reference's
+    graphio.load_edge_list contract, graphio.py:143-191: same errors, a
+    trailing weight ignored unless ``weighted``, ids from 0)."""
+    cols = _Columns(weighted)
+    for lineno, toks in _records(path):
+        where = "%s:%d" % (path, lineno)
+        if len(toks) < 2:
+            raise GraphLoadError("%s: malformed edge line %r" % (where, " ".join(toks)))
+        try:
+            u, v = int(toks[0]), int(toks[1])
+        except ValueError:
+            raise GraphLoadError("%s: non-integer vertex id in %r"
+                                 % (where, " ".join(toks))) from None
+        if min(u, v) < 0:
+            raise GraphLoadError("%s: negative vertex id" % where)
+        w = None
+        if weighted:
+            if len(toks) < 3:
+                raise GraphLoadError("%s: missing weight token" % where)
+            w = _as_int(toks[2], where, "weight")
+            if w < 0:
+                raise GraphLoadError("%s: negative weight" % where)
+        cols.add(u, v, w)
+    if not cols.src:
         raise GraphLoadError("%s: no edges" % path)
-    diag = {"comment_lines": comments, "input_edges": len(src)}
+    s, d, w = cols.arrays()
+    diag = {"comment_lines": _count_comments(path), "input_edges": len(s)}
     if symmetrize:
-        src, dst, wts, dropped = symmetrize_coo(src, dst, wts)
-        diag["duplicates_collapsed"] = dropped
-    n = int(max(max(src), max(dst))) + 1
-    return Graph.from_coo(n, src, dst, wts, symmetric=symmetrize, diagnostics=diag,
-                          device=device)
+        s, d, w, diag["duplicates_collapsed"] = symmetrize_coo(s, d, w)
+    n = int(max(s.max(), d.max())) + 1
+    return Graph.from_coo(n, s, d, w, symmetric=symmetrize, diagnostics=diag, device=device)
 
 
 def load_matrix_market(path, weighted=False, device=0):
-    """MatrixMarket coordinate file (graphio.py:193-261): 1-based ids, a
-    'symmetric' banner mirrors every off-diagonal entry, integer values as
-    weights; the declared dimensions bound the ids."""
+    """MatrixMarket coordinate file (graphio.py:193-261 contract): 1-based
+    ids, a 'symmetric' banner mirrors off-diagonal entries, integer values
+    are weights, the size line bounds the ids."""
     with open(path) as fh:
         banner = fh.readline()
-        if not banner.startswith("%%MatrixMarket matrix coordinate"):
-            raise GraphLoadError("%s: not a MatrixMarket coordinate file" % path)
-        tok = banner.strip().lower().split()
-        fld = tok[3] if len(tok) > 3 else "pattern"
-        symmetric = len(tok) > 4 and tok[4] == "symmetric"
-        if weighted and fld == "pattern":
-            raise GraphLoadError("%s: pattern matrix has no weights" % path)
-        lineno, dims = 1, None
-        src, dst, wts = [], [], ([] if weighted else None)
-        for raw in fh:
-            lineno += 1
-            line = raw.strip()
-            if not line or line[0] == "%":
-                continue
-            parts = line.split()
-            if dims is None:
-                if len(parts) != 3:
-                    raise GraphLoadError("%s:%d: bad size line %r" % (path, lineno, line))
-                dims = [int(x) for x in parts]
-                if dims[0] != dims[1]:
-                    raise GraphLoadError("%s: adjacency matrix must be square" % path)
-                continue
-            if len(parts) < 2:
-                raise GraphLoadError("%s:%d: malformed entry %r" % (path, lineno, line))
-            i, j = int(parts[0]) - 1, int(parts[1]) - 1
-            if i < 0 or j < 0:
-                raise GraphLoadError("%s:%d: ids are 1-based" % (path, lineno))
-            if weighted:
-                if len(parts) < 3:
-                    raise GraphLoadError("%s:%d: missing value token" % (path, lineno))
-                val = float(parts[2])
-                if val != int(val) or val < 0:
-                    raise GraphLoadError("%s:%d: weights must be non-negative integers"
-                                         % (path, lineno))
-            pairs = [(i, j)] + ([(j, i)] if symmetric and i != j else [])
-            for a, b in pairs:
-                src.append(a)
-                dst.append(b)
-                if weighted:
-                    wts.append(int(val))
-    if dims is None:
+    if not banner.startswith("%%MatrixMarket matrix coordinate"):
+        raise GraphLoadError("%s: not a MatrixMarket coordinate file" % path)
+    head = banner.lower().split()
+    value_field = head[3] if len(head) > 3 else "pattern"
+    mirror = len(head) > 4 and head[4] == "symmetric"
+    if weighted and value_field == "pattern":
+        raise GraphLoadError("%s: pattern matrix has no weights" % path)
+    rows = None
+    cols = _Columns(weighted)
+    for lineno, toks in _records(path, skip_first=True):
+        where = "%s:%d" % (path, lineno)
+        if rows is None:  # the size line
+            if len(toks) != 3:
+                raise GraphLoadError("%s: bad size line %r" % (where, " ".join(toks)))
+            rows, ncols, nnz = (int(x) for x in toks)
+            if rows != ncols:
+                raise GraphLoadError("%s: adjacency matrix must be square" % path)
+            continue
+        if len(toks) < 2:
+            raise GraphLoadError("%s: malformed entry %r" % (where, " ".join(toks)))
+        i, j = int(toks[0]) - 1, int(toks[1]) - 1
+        if min(i, j) < 0:
+            raise GraphLoadError("%s: ids are 1-based" % where)
+        w = None
+        if weighted:
+            if len(toks) < 3:
+                raise GraphLoadError("%s: missing value token" % where)
+            val = float(toks[2])
+            if val < 0 or val != int(val):
+                raise GraphLoadError("%s: weights must be non-negative integers" % where)
+            w = int(val)
+        cols.add(i, j, w)
+        if mirror and i != j:
+            cols.add(j, i, w)
+    if rows is None:
         raise GraphLoadError("%s: missing size line" % path)
-    if not src:
+    if not cols.src:
         raise GraphLoadError("%s: no edges" % path)
-    n = dims[0]
-    if max(max(src), max(dst)) >= n:
+    s, d, w = cols.arrays()
+    if max(s.max(), d.max()) >= rows:
         raise GraphLoadError("%s: entry outside declared dimensions" % path)
-    return Graph.from_coo(n, src, dst, wts, symmetric=symmetric,
-                          diagnostics={"declared_nnz": dims[2]}, device=device)
+    return Graph.from_coo(rows, s, d, w, symmetric=mirror, diagnostics={"declared_nnz": nnz},
+                          device=device)
 
 
 def load_graph(path, weighted=False, symmetrize=False, device=0):
-    """MatrixMarket banner or plain edge list (graphio.py:264-278)."""
+    """Dispatch on the first line: MatrixMarket banner or plain edge list
+    (graphio.py:264-278)."""
     with open(path) as fh:
-        first = fh.readline()
-    if first.startswith("%%MatrixMarket"):
-        g = load_matrix_market(path, weighted=weighted, device=device)
-        if symmetrize and not g.symmetric:
-            s, d, w, dropped = symmetrize_coo(g.coo_src, g.coo_dst, g.coo_weights)
-            g = Graph.from_coo(g.num_vertices, s, d, w, symmetric=True,
-                               diagnostics=dict(g.diagnostics, duplicates_collapsed=dropped),
-                               device=device)
-        return g
-    return load_edge_list(path, weighted=weighted, symmetrize=symmetrize, device=device)
+        is_mm = fh.readline().startswith("%%MatrixMarket")
+    if not is_mm:
+        return load_edge_list(path, weighted=weighted, symmetrize=symmetrize, device=device)
+    g = load_matrix_market(path, weighted=weighted, device=device)
+    if symmetrize and not g.symmetric:
+        s, d, w, dropped = symmetrize_coo(g.coo_src, g.coo_dst, g.coo_weights)
+        g = Graph.from_coo(g.num_vertices, s, d, w, symmetric=True,
+                           diagnostics=dict(g.diagnostics, duplicates_collapsed=dropped),
+                           device=device)
+    return g
 
 
 def with_random_weights(g, low=1, high=1000, seed=0):

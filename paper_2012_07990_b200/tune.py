@@ -7,10 +7,12 @@ variants for sssp), optionally shuffled and truncated -- but every trial runs
 on the device and is timed by the library's CUDA events
 (``RunStats.kernel_ms``), median of ``repeats`` runs after ``warmup``.
 
-The reference's ``--check`` compares each trial with its CPU oracle; the
-product path has no CPU implementation, so ``check=True`` compares each trial
-with the default schedule's device result instead (BFS levels, CC labels and
-SSSP distances exactly, PageRank within 1e-6 and BC within 1e-5 relative).
+``check=True`` is the reference's ``--check`` (cli.py:262-270): every trial
+is compared with the independent host checker (``checkers``, the reference's
+oracle.py) when the graph is within its size guard, or with a caller-supplied
+``expected`` answer; past the guard with no ``expected``, trials are compared
+with the default schedule's device result (BFS levels, CC labels and SSSP
+distances exactly, PageRank within 1e-6 and BC within 1e-5 relative).
 """
 
 from __future__ import annotations
@@ -23,7 +25,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import algos
+from . import algos, checkers
 from .sched import Schedule, ScheduleError, ScheduleProgram, enumerate_space, pretty_print
 
 # cli.py:21-29
@@ -124,17 +126,27 @@ class TuneResult:
                 fh.write(pretty_print(self.best_program))
 
 
+def _check_values(algo, result):
+    a = np.asarray(result.array)
+    return a.tolist()
+
+
 def tune(algo, g, budget_s=60.0, *, source=0, sources=None, max_iters=20, exec_cfg=None,
          seed=0, strategy="exhaustive", limit=None, deltas=None, warmup=1, repeats=3,
-         check=False):
+         check=False, expected=None):
     """Time every candidate on the device within ``budget_s`` seconds (the
-    first candidate always runs); the fastest median wins."""
+    first candidate always runs); the fastest median wins, among trials that
+    pass the check when ``check`` is set.  ``expected``: the answer to check
+    against, in ``checkers.compare`` form (levels for bfs, inf for sssp)."""
     if budget_s <= 0:
         raise ValueError("budget must be positive (seconds)")
     sources = list(sources) if sources is not None else [source]
     cands = candidate_schedules(algo, seed=seed, strategy=strategy, limit=limit, deltas=deltas)
     res = TuneResult(None, None, candidates=len(cands))
     reference = None
+    if check and expected is None and g.num_vertices <= checkers.ORACLE_MAX_VERTICES:
+        expected = checkers.expected(algo, g, source=source, sources=sources,
+                                     max_iters=max_iters, tolerance=0.0)
     t0 = time.perf_counter()
     for idx, cand in enumerate(cands):
         if idx > 0 and time.perf_counter() - t0 > budget_s:
@@ -153,7 +165,10 @@ def tune(algo, g, budget_s=60.0, *, source=0, sources=None, max_iters=20, exec_c
             continue
         med = statistics.median(times)
         ok = ""
-        if check:
+        if check and expected is not None:
+            ok = "true" if checkers.compare(algo, _check_values(algo, result), expected)[0] \
+                else "false"
+        elif check:
             if reference is None:
                 reference = result
                 ok = "true"

@@ -1,5 +1,7 @@
 """Device graph construction vs the reference layout (graphio.from_coo)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -102,3 +104,43 @@ def test_sidecar_straight_to_device(tmp_path):
     g4 = gg.Graph.from_coo(g.num_vertices, g.coo_src, g.coo_dst, g.coo_weights)
     with pytest.raises(ValueError):
         load_blocked_to_device(str(tmp_path / "bad.blk"), g4)
+
+
+@pytest.mark.gpu
+def test_reference_written_sidecar_to_device():
+    """A sidecar written by the reference's save_blocked (tests/golden) is
+    installed on the device as the graph's Alg. 1 layout; the device's own
+    Alg. 1 on the same COO writes a byte-identical sidecar, and EdgeBlocking
+    PageRank on the installed layout matches the oracle."""
+    import glob
+    import tempfile
+    import oracle
+    from oracle import gen
+    from tests.conftest import GOLDEN
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.blocking import block_edges, load_blocked_to_device, save_blocked
+    V, s, d = gen.rmat(8, 4, seed=11)
+    w = gen.weights(len(s), 11)
+    want_pr, _ = oracle.pagerank(V, s, d, 15, 0.0)
+    paths = sorted(glob.glob(os.path.join(GOLDEN, "ref_sidecar_*.blk")))
+    assert len(paths) == 3
+    for path in paths:
+        weighted = "unweighted" not in path
+        g = load_blocked_to_device(path)            # graph built from the sidecar's edges
+        fresh = gg.Graph.from_coo(V, s, d, w if weighted else None)
+        n = int(path.rsplit("_n", 1)[1].split(".")[0])
+        with tempfile.TemporaryDirectory() as tmp:
+            out = os.path.join(tmp, "dev.blk")
+            save_blocked(block_edges(fresh, n), out)
+            assert open(out, "rb").read() == open(path, "rb").read()
+        g2 = gg.Graph.from_coo(V, s, d, w if weighted else None)
+        load_blocked_to_device(path, g2)            # installed into an existing graph
+        import torch
+        for graph in (g, g2):  # Alg. 2 over the installed layout (no Alg. 1 rerun)
+            counts = torch.zeros(V, dtype=torch.int64, device="cuda")
+            assert gg.apply_blocked((graph, n), gg.udfs.CountInDegree(counts)) == len(s)
+            assert np.array_equal(counts.cpu().numpy(), np.bincount(d, minlength=V))
+            prog = gg.ScheduleProgram({"s0:s1": gg.Schedule(load_balance="EDGE_ONLY",
+                                                            blocking=True, blocking_size=n)})
+            r = gg.pagerank(graph, prog, max_iters=15, tolerance=0.0).array
+            assert np.max(np.abs(r - want_pr) / want_pr) < 1e-12

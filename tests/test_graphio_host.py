@@ -2,6 +2,8 @@
 on the host before any device call, so they run without a GPU; the
 successful loads are GPU tests."""
 
+import os
+
 import pytest
 
 from paper_2012_07990_b200.graphio import (GraphLoadError, load_edge_list, load_graph,
@@ -68,3 +70,38 @@ def test_matrix_market_general_and_symmetric(tmp_path):
     g = load_graph(write(tmp_path, "%%MatrixMarket matrix coordinate pattern general\n"
                                    "3 3 1\n1 2\n", "t.mtx"), symmetrize=True)
     assert g.symmetric and g.num_edges == 2
+
+
+# ---------------------------------------------------------------------------
+# sidecars written by the reference's own save_blocked (oracle/make_golden.py
+# sidecars(), blocking.py:189-217): read them, and write byte-identical files
+# ---------------------------------------------------------------------------
+def _ref_sidecars():
+    import glob
+    from tests.conftest import GOLDEN
+    return sorted(glob.glob(os.path.join(GOLDEN, "ref_sidecar_*.blk")))
+
+
+def test_reference_sidecars_round_trip_byte_identical(tmp_path):
+    import numpy as np
+    import oracle
+    from oracle import gen
+    from paper_2012_07990_b200.blocking import BlockedGraph, load_blocked, save_blocked
+    paths = _ref_sidecars()
+    assert len(paths) == 3
+    V, s, d = gen.rmat(8, 4, seed=11)
+    w = gen.weights(len(s), 11)
+    for path in paths:
+        bg = load_blocked(path)
+        n = bg.vertices_per_segment
+        weighted = "unweighted" not in path
+        # the same layout from the oracle's Alg. 1 on the same COO
+        perm, seg = oracle.block_edges(V, d, n)
+        assert bg.segment_start == seg.tolist()
+        assert bg.edges_src == s[perm].tolist() and bg.edges_dst == d[perm].tolist()
+        assert bg.edges_weight == (w[perm].astype(int).tolist() if weighted else None)
+        mine = BlockedGraph(V, n, seg.tolist(), s[perm].tolist(), d[perm].tolist(),
+                            w[perm].astype(int).tolist() if weighted else None)
+        out = tmp_path / "mine.blk"
+        save_blocked(mine, str(out))
+        assert out.read_bytes() == open(path, "rb").read()
