@@ -78,7 +78,8 @@ def parse():
     p.add_argument("--fusion", action="store_true", help="c1/c2/c5: fused loop (s0 kernel fusion)")
     p.add_argument("--side", type=int, default=None, help="c3 grid side")
     p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")
-    p.add_argument("--lb", default="WM", help="c3 load balance (swept: WM best)")
+    p.add_argument("--lb", default="VERTEX_BASED",
+                   help="c3 load balance (VERTEX_BASED runs the asynchronous bucket phases; swept best)")
     p.add_argument("--no-fusion", action="store_true", help="c3: unfused loop")
     p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED,EB,EDGE,HYBRID",
                    help="c4 load balances (EB = EDGE_ONLY+BLOCKED, EDGE = EDGE_ONLY)")

@@ -329,7 +329,7 @@ def sssp_c3(gg, args, peak):
     g = gg.generate_grid(side, seed=4, weights=True)
     gen_s = time.perf_counter() - t0
     V, A = g.num_vertices, g.num_edges
-    deltas = [args.delta] if args.delta else [4096, 8192, 16384, 32768]
+    deltas = [args.delta] if args.delta else [4096, 8192, 16384]
     dist = torch.empty(V, dtype=torch.int64, device="cuda")
 
     def program(d):

@@ -436,3 +436,38 @@ def test_staged_output_overflow(gg, dedup):
     assert gg.bfs_levels(r.values) == oracle.bfs_levels(V, off, nbr, 0).tolist()
     assert r.stats.edges_traversed == int(sum(np.diff(off)[np.asarray(r.values) >= 0]))
     legal_bfs_tree(g, r.values, 0)
+
+
+# ---------------------------------------------------------------------------
+# fused VERTEX_BASED delta-stepping: asynchronous bucket phases (sssp.cu
+# k_sssp_async) -- exact distances for every bucket width, the work-list
+# spill into the global ring, and the reference's round count at delta 1
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("delta", [1, 7, 100, 5000, 1 << 30])
+@pytest.mark.parametrize("spill", [None, "32"])
+def test_sssp_async_phases_match_oracle(gg, delta, spill, monkeypatch):
+    if spill:
+        monkeypatch.setenv("GG_SSSP_SPILL", spill)  # most in-bucket pushes go through the ring
+        monkeypatch.setenv("GG_SSSP_PULL", "3")
+    g = gg.generate_grid(96, seed=11)
+    V = g.num_vertices
+    off, nbr, w = oracle.csr(V, g.coo_src, g.coo_dst, g.coo_weights)
+    want, rounds = oracle.sssp_delta(V, off, nbr, w, 5, delta)
+    r = gg.sssp_delta(g, 5, program_with(gg.Schedule(load_balance="VERTEX_BASED", delta=delta), True))
+    assert np.array_equal(r.array, want)
+    assert r.stats.dispatch_count == 1
+    if delta == 1:
+        assert r.stats.rounds == rounds
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_sssp_async_rmat_hubs(gg, seed):
+    # hubs (thousands of arcs) walked by lane groups; unreachable vertices stay inf
+    V, s, d = gen.rmat(12, 8, seed=seed)
+    w = gen.weights(len(s), seed + 10)
+    g = gg.Graph.from_coo(V, s, d, w)
+    off, nbr, ww = oracle.csr(V, s, d, w)
+    for delta in (3, 50, 2000):
+        want, _ = oracle.sssp_delta(V, off, nbr, ww, 0, delta)
+        r = gg.sssp_delta(g, 0, program_with(gg.Schedule(load_balance="VERTEX_BASED", delta=delta), True))
+        assert np.array_equal(r.array, want), delta
