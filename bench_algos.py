@@ -422,6 +422,9 @@ def cc_bc_c4(gg, args, peak):
     labels = torch.empty(V, dtype=torch.int32, device="cuda")
     scores = torch.empty(V, dtype=torch.float64, device="cuda")
     bc_sources = _pick_sources(deg, args.sources or 4, 6)
+    # the degree-ordered copy CC/BC query on (relabel.cu), built ahead like
+    # the EdgeBlocking layout: preprocessing, reported apart
+    relabel_ms = g.prepare_relabel() if os.environ.get("GG_RELABEL", "1") != "0" else 0.0
 
     # oracle results first (parity for every load balancer below)
     t0 = time.perf_counter()
@@ -515,7 +518,10 @@ def cc_bc_c4(gg, args, peak):
                        "coo_order": "by source (edge-list order; matters for EDGE_ONLY/EB only)",
                        "headline": "CC %s (GTEPS = A x hooking rounds / time)" % head,
                        "cc": cc_res, "bc": bc_res, "bc_sources": bc_sources,
-                       "bc_m_c": m_c, "generate_s": gen_s},
+                       "bc_m_c": m_c, "generate_s": gen_s,
+                       "relabel_prep_ms": relabel_ms,
+                       "relabel": "degree-descending copy (GG_RELABEL=%s)"
+                                  % os.environ.get("GG_RELABEL", "default: on for V >= 2^20")},
             "roofline": dict(_roof((4.0 * A + 16.0 * V) * cc_res[head]["rounds"], ms, peak),
                              note="B_alg = (4*A + 16*V) per hooking round (SURVEY 8d)"),
             "e2e": {"value": st.edges_traversed / e2e_s / 1e9, "unit": "GTEPS",

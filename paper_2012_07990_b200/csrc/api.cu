@@ -660,9 +660,25 @@ int gg_bfs(const gg_graph* g, int64_t source, const gg_binding* binding, int32_t
   NEED(binding);
   NEED(parents);
   DeviceGuard guard(g->g->dev);
-  Runtime rt(g->g.get(), cfg);
+  // locality relabelling (relabel.cu): the query runs on the degree-ordered
+  // copy and the parents map back (an invalid source passes through so the
+  // driver reports it)
+  std::shared_ptr<Relabel> R;
+  const Graph* gp = g->g.get();
+  if (relabel_wanted(*gp, kRelabelBfs)) {
+    R = relabel_for(*gp);
+    gp = relabel_graph(*R);
+  }
+  Runtime rt(gp, cfg);
   CallTimer t(g->g->dev);
-  bfs_run(*g->g, source, *binding, fusion != 0, rt, parents);
+  if (R) {
+    const int64_t s2 = source >= 0 && source < gp->V ? relabel_vertex(*R, source) : source;
+    DevBuf<int32_t> tmp(std::max<int64_t>(gp->V, 1));
+    bfs_run(*gp, s2, *binding, fusion != 0, rt, tmp.p);
+    relabel_parents_out(*R, tmp.p, parents, rt.stream);
+  } else {
+    bfs_run(*gp, source, *binding, fusion != 0, rt, parents);
+  }
   t.finish(g->g->dev, rt, stats);
   GG_API_END
 }
@@ -688,9 +704,21 @@ int gg_cc(const gg_graph* g, const gg_binding* binding, int32_t fusion, const gg
   NEED(binding);
   NEED(labels);
   DeviceGuard guard(g->g->dev);
-  Runtime rt(g->g.get(), cfg);
+  std::shared_ptr<Relabel> R;  // locality relabelling (relabel.cu)
+  const Graph* gp = g->g.get();
+  if (relabel_wanted(*gp, kRelabelCc)) {
+    R = relabel_for(*gp);
+    gp = relabel_graph(*R);
+  }
+  Runtime rt(gp, cfg);
   CallTimer t(g->g->dev);
-  cc_run(*g->g, *binding, fusion != 0, rt, labels);
+  if (R) {  // canonical labels: each component's minimum ORIGINAL id
+    DevBuf<int32_t> tmp(std::max<int64_t>(gp->V, 1));
+    cc_run(*gp, *binding, fusion != 0, rt, tmp.p);
+    relabel_cc_out(*R, tmp.p, labels, rt.stream);
+  } else {
+    cc_run(*gp, *binding, fusion != 0, rt, labels);
+  }
   t.finish(g->g->dev, rt, stats);
   GG_API_END
 }
@@ -703,10 +731,34 @@ int gg_bc(const gg_graph* g, const int64_t* sources, int64_t num_sources, const 
   NEED(scores);
   if (num_sources > 0) NEED(sources);
   DeviceGuard guard(g->g->dev);
-  Runtime rt(g->g.get(), cfg);
+  std::shared_ptr<Relabel> R;  // locality relabelling (relabel.cu)
+  const Graph* gp = g->g.get();
+  if (relabel_wanted(*gp, kRelabelBc)) {
+    R = relabel_for(*gp);
+    gp = relabel_graph(*R);
+  }
+  Runtime rt(gp, cfg);
   CallTimer t(g->g->dev);
-  bc_run(*g->g, sources, num_sources, *binding, rt, scores);
+  if (R) {
+    std::vector<int64_t> s2(num_sources > 0 ? num_sources : 0);
+    for (int64_t k = 0; k < num_sources; ++k)  // invalid ones pass through: the driver reports them
+      s2[k] = sources[k] >= 0 && sources[k] < gp->V ? relabel_vertex(*R, sources[k]) : sources[k];
+    DevBuf<double> tmp(std::max<int64_t>(gp->V, 1));
+    bc_run(*gp, s2.data(), num_sources, *binding, rt, tmp.p);
+    relabel_scores_out(*R, tmp.p, scores, rt.stream);
+  } else {
+    bc_run(*gp, sources, num_sources, *binding, rt, scores);
+  }
   t.finish(g->g->dev, rt, stats);
+  GG_API_END
+}
+
+int gg_relabel_prepare(const gg_graph* g, double* prep_ms) {
+  GG_API_BEGIN
+  NEED(g);
+  DeviceGuard guard(g->g->dev);
+  auto R = relabel_for(*g->g);
+  if (prep_ms) *prep_ms = relabel_prep_ms(*R);
   GG_API_END
 }
 

@@ -32,6 +32,7 @@ struct Graph {
   std::shared_ptr<PullPlan> pull_plan;
   std::shared_ptr<void> pr_block;  // PageRank EdgeBlocking layout (prblock.cu)
   std::shared_ptr<void> pr_tiles;  // merge-path tile plan over CSR-in (pagerank.cu)
+  std::shared_ptr<void> relabel;   // degree-ordered copy for CC / BC / BFS (relabel.cu)
   // CSR views are built on first use (a schedule that only streams the COO
   // never pays for the transpose); guarded by view_mu.
   bool has_out = false, has_in = false;
@@ -73,5 +74,18 @@ void stable_order(int dev, const int32_t* keys, int64_t n, int64_t key_limit, De
 // offsets[k] = first position of key >= k in sorted keys (length nkeys+1).
 void offsets_from_sorted(int dev, const int32_t* sorted, int64_t n, int64_t nkeys, int64_t* off,
                          cudaStream_t s);
+
+// Locality relabelling (relabel.cu): the graph renumbered by degree,
+// descending, for the frontier algorithms; results map back to original ids.
+struct Relabel;
+constexpr int kRelabelCc = 0, kRelabelBc = 1, kRelabelBfs = 2;
+bool relabel_wanted(const Graph& g, int algo);
+std::shared_ptr<Relabel> relabel_for(const Graph& g);
+const Graph* relabel_graph(const Relabel& R);
+double relabel_prep_ms(const Relabel& R);
+int32_t relabel_vertex(const Relabel& R, int64_t v);  // original id -> new id
+void relabel_cc_out(const Relabel& R, const int32_t* labels_new, int32_t* out, cudaStream_t st);
+void relabel_parents_out(const Relabel& R, const int32_t* par_new, int32_t* out, cudaStream_t st);
+void relabel_scores_out(const Relabel& R, const double* x_new, double* out, cudaStream_t st);
 
 }  // namespace gg

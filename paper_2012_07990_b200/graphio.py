@@ -141,6 +141,14 @@ class Graph:
         """Free the COO view on the device (CSR views stay)."""
         _lib.call("gg_graph_drop_coo", self._h)
 
+    def prepare_relabel(self):
+        """Build the degree-ordered copy that cc_soman / bc query on large
+        graphs (relabel.cu; cached on the graph) ahead of the queries and
+        return its preprocessing time in ms."""
+        ms = C.c_double(0.0)
+        _lib.call("gg_relabel_prepare", self._h, C.byref(ms))
+        return ms.value
+
 
 def out_degree(g, v):
     if not 0 <= v < g.num_vertices:
