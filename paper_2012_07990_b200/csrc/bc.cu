@@ -28,6 +28,23 @@ __global__ void k_bc_accumulate(const double* delta, double* score, int64_t V, i
     if (v != s) score[v] += delta[v];
 }
 
+// bc_run's array-of-structs state (ops.cuh BcState): init and accumulate
+__global__ void k_bc_init_aos(BcState* st, int64_t V, int64_t s) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    BcState x{};
+    x.sigma = v == s ? 1.0 : 0.0;
+    x.delta = 0.0;
+    x.depth = v == s ? 0 : -1;
+    st[v] = x;
+  }
+}
+__global__ void k_bc_accumulate_aos(const BcState* st, double* score, int64_t V, int64_t s) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
+       v += (int64_t)gridDim.x * blockDim.x)
+    if (v != s) score[v] += st[v].delta;
+}
+
 __global__ void k_halve(double* score, int64_t V) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
        v += (int64_t)gridDim.x * blockDim.x)
@@ -93,13 +110,14 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
   bwd.s1 = b.s1;  // (bound.s1 if hybrid else bound).copy(), direction PUSH
   bwd.s1.direction = GG_PUSH;
   bwd.s2 = bwd.s1;
-  DevBuf<int32_t> depth(V), order(V + 1);
-  DevBuf<double> sigma(V), delta(V), score(V);
+  DevBuf<BcState> state(std::max<int64_t>(V, 1));  // depth, sigma, delta per vertex: one sector
+  DevBuf<int32_t> order(V + 1);
+  DevBuf<double> score(V);
   DevBuf<unsigned long long> nsel(1);
   score.zero(st);
   for (int64_t si = 0; si < nsrc; ++si) {
     const int64_t s = sources[si];
-    k_bc_init<<<grid_for(V, 256, dev), 256, 0, st>>>(depth.p, sigma.p, delta.p, V, s);
+    k_bc_init_aos<<<grid_for(V, 256, dev), 256, 0, st>>>(state.p, V, s);
     GG_LAUNCH_CHECK();
     count_launch();
     int32_t s32 = (int32_t)s;
@@ -110,7 +128,7 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
     while (frontier_size(&rt, frontier.get()) > 0) {
       pos += snapshot(rt, frontier.get(), order.p, pos, nsel);
       level_start.push_back(pos);
-      OpBcFwd op{depth.p, sigma.p, level};
+      OpBcFwdAoS op{state.p, level};
       rt.edge_begin();
       std::unique_ptr<Frontier> out = apply_op(&rt, op, true, &frontier, b, true, true);
       rt.edge_end();
@@ -120,7 +138,7 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
     }
     rt.release(std::move(frontier));
     const int64_t nrounds = (int64_t)level_start.size() - 1;
-    OpBcBwd bop{depth.p, sigma.p, delta.p};
+    OpBcBwdAoS bop{state.p};
     for (int64_t r = nrounds - 2; r >= 0; --r) {
       const int64_t lo = level_start[r], cnt = level_start[r + 1] - lo;
       std::unique_ptr<Frontier> wave = rt.acquire(GG_SPARSE);  // new_frontier(n, rounds[r])
@@ -133,7 +151,7 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
       rt.edge_end();
       rt.stats.rounds += 1;
     }
-    k_bc_accumulate<<<grid_for(V, 256, dev), 256, 0, st>>>(delta.p, score.p, V, s);
+    k_bc_accumulate_aos<<<grid_for(V, 256, dev), 256, 0, st>>>(state.p, score.p, V, s);
     GG_LAUNCH_CHECK();
     count_launch();
   }

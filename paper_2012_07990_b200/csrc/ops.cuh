@@ -254,4 +254,75 @@ struct OpBcBwd {
   __device__ __forceinline__ void finish(int32_t, const Acc&, const OutBuilder&) const {}
 };
 
+// The same two rounds over an array-of-structs state (bc_run's own layout):
+// depth, sigma and delta of a vertex share one 32-byte sector, so the
+// backward round's three random gathers per arc (depth[v], sigma[v],
+// delta[v]) are one sector, and the forward round's depth test, CAS and
+// sigma add hit one line.  The UDF boundary (gg_edgeset_apply) keeps the
+// reference's separate arrays (OpBcFwd / OpBcBwd above).
+struct __align__(32) BcState {
+  double sigma;
+  double delta;
+  int32_t depth;
+  int32_t pad[3];
+};
+struct OpBcFwdAoS {
+  BcState* st;
+  int32_t level;
+  using Acc = BcAcc;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t v) const {
+    const int32_t d = *((volatile int32_t*)&st[v].depth);
+    return d == -1 || d == level + 1;
+  }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder& out) const {
+    const int32_t nl = level + 1;
+    if (*((volatile int32_t*)&st[v].depth) == -1 && atomicCAS(&st[v].depth, -1, nl) == -1) out.emit(v);
+    if (*((volatile int32_t*)&st[v].depth) == nl) atomicAdd(&st[v].sigma, st[u].sigma);
+  }
+  __device__ __forceinline__ Acc init() const { return {0.0, 0}; }
+  __device__ __forceinline__ bool visit(Acc& a, int32_t, int32_t u, uint32_t) const {
+    a.s += st[u].sigma;
+    a.found = 1;
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc b) { return {a.s + b.s, a.found | b.found}; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return OpBcFwd::warp_reduce(a); }
+  __device__ __forceinline__ void finish(int32_t v, const Acc& a, const OutBuilder& out) const {
+    if (!a.found) return;
+    if (st[v].depth == -1) {
+      st[v].depth = level + 1;
+      out.emit(v);
+    }
+    st[v].sigma += a.s;
+  }
+};
+struct OpBcBwdAoS {
+  BcState* st;
+  using Acc = int;
+  static constexpr bool kEarlyExit = false;
+  __device__ __forceinline__ bool filter(int32_t) const { return true; }
+  __device__ __forceinline__ double contrib(int32_t u, int32_t v) const {
+    // one 32-byte load of v's state (depth, sigma, delta); u's is per range
+    const double2 sd = __ldg(reinterpret_cast<const double2*>(&st[v]));  // v's state is final
+    const int32_t dv = __ldg(&st[v].depth);                               // (same sector: L1 hit)
+    return dv == __ldg(&st[u].depth) + 1 ? __ldg(&st[u].sigma) / sd.x * (1.0 + sd.y) : 0.0;
+  }
+  __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
+    const double x = contrib(u, v);
+    if (x != 0.0) atomicAdd(&st[u].delta, x);
+  }
+  static constexpr bool kPushReduce = true;
+  __device__ __forceinline__ double push_val(int32_t u, int32_t v) const { return contrib(u, v); }
+  __device__ __forceinline__ void push_commit(int32_t u, double x) const { atomicAdd(&st[u].delta, x); }
+  __device__ __forceinline__ Acc init() const { return 0; }
+  __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t w) const {
+    push(u, v, w, OutBuilder{});
+    return false;
+  }
+  static __device__ __forceinline__ Acc combine(Acc a, Acc) { return a; }
+  static __device__ __forceinline__ Acc warp_reduce(Acc a) { return a; }
+  __device__ __forceinline__ void finish(int32_t, const Acc&, const OutBuilder&) const {}
+};
+
 }  // namespace gg
