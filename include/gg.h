@@ -358,6 +358,11 @@ int gg_bfs_dist(gg_comm* c, const gg_graph* g, int64_t source, double threshold,
 /* The vertex partition gg_bfs_dist uses (nranks+1 entries). */
 int gg_bfs_dist_bounds(const gg_graph* g, int32_t nranks, int64_t* bounds);
 /* The same with `nparts` virtual ranks on the graph's one device (test mode). */
+/* Bytes one rank received through the exchange in the last gg_bfs_dist /
+ * gg_bfs_virtual call on this thread (top-down: V/8 of discovered bitmap
+ * slices, bottom-up: V/8 of frontier words, per level; plus the final
+ * V*4-byte parent all-gather). */
+int gg_last_exchange_bytes(uint64_t* bytes);
 int gg_bfs_virtual(const gg_graph* g, int32_t nparts, int64_t source, double threshold,
                    int32_t* parents, gg_stats* stats);
 /* Test mode of the partitioned run: `nparts` virtual ranks on the graph's

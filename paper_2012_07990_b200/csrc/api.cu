@@ -7,6 +7,9 @@
 namespace gg {
 static thread_local std::string t_err;
 static thread_local int64_t t_launches = 0;
+static thread_local uint64_t t_exchange_bytes = 0;
+void set_exchange_bytes(uint64_t b) { t_exchange_bytes = b; }
+uint64_t last_exchange_bytes() { return t_exchange_bytes; }
 void set_last_error(const std::string& m) { t_err = m; }
 void count_launch(int n) { t_launches += n; }
 int64_t launches_now() { return t_launches; }
@@ -842,6 +845,13 @@ int gg_bfs_dist_bounds(const gg_graph* g, int32_t nranks, int64_t* bounds) {
   DeviceGuard guard(g->g->dev);
   std::vector<int64_t> b = bfsd_bounds(*g->g, nranks, 0);
   memcpy(bounds, b.data(), (nranks + 1) * sizeof(int64_t));
+  GG_API_END
+}
+
+int gg_last_exchange_bytes(uint64_t* bytes) {
+  GG_API_BEGIN
+  NEED(bytes);
+  *bytes = last_exchange_bytes();
   GG_API_END
 }
 

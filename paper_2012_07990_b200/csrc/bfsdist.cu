@@ -8,10 +8,14 @@
 // bitmap.  Per level, with the same hybrid rule as the single-GPU path
 // (PULL iff |frontier| > threshold * V, engine.py:632):
 //   top-down:  each rank expands the frontier vertices it owns over their
-//              out-arcs, proposing cand[v] = max(u) for unvisited v; the
-//              exchange is an all-reduce(max) of cand; every rank then marks
-//              the discovered set (identical everywhere) and owners take
-//              parent[v] = cand[v] (a frontier neighbour: a legal BFS parent);
+//              out-arcs and sets the bits of unvisited targets in a V-bit
+//              discovered bitmap; the exchange is an all-to-all of bitmap
+//              slices OR-ed at their owners (V/8 bytes per rank, not the
+//              4*V-byte parent-candidate all-reduce of the first version);
+//              each owner then gives its newly discovered vertices a parent
+//              from the replicated frontier bitmap (first in-arc from the
+//              frontier: a legal BFS parent) and all-gathers its owned words
+//              of the next frontier;
 //   bottom-up: each rank scans the in-arcs of its owned unvisited vertices
 //              against the replicated frontier bitmap (first hit wins, which
 //              is the reference's pull semantics: later arcs are no-ops once
@@ -25,12 +29,10 @@
 
 namespace gg {
 
-__global__ void k_bfsd_init(int32_t* parent, int32_t* cand, int64_t V, uint32_t* vis, uint32_t* fr, uint32_t* nx,
-                            int64_t W, int32_t source) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void k_bfsd_init(int32_t* parent, int64_t V, uint32_t* vis, uint32_t* fr, uint32_t* nx, int64_t W,
+                            int32_t source) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
     parent[i] = i == source ? source : -1;
-    cand[i] = -1;
-  }
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W; w += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t b = (w == (source >> 5)) ? (1u << (source & 31)) : 0u;
     vis[w] = b;
@@ -55,10 +57,11 @@ __global__ void k_bfsd_queue(const uint32_t* fr, int64_t w0, int64_t w1, int32_t
   }
 }
 
-// top-down: warp per queued vertex, lanes over its out-arcs
-__global__ void __launch_bounds__(256) k_bfsd_push(const int64_t* off, const int32_t* nbr, const int32_t* q,
-                                                   const unsigned long long* qn, const uint32_t* vis, int32_t* cand,
-                                                   unsigned long long* scanned) {
+// top-down, bitmap form: warp per queued vertex, unvisited targets set their
+// bit in this rank's discovered bitmap
+__global__ void __launch_bounds__(256) k_bfsd_push_bm(const int64_t* off, const int32_t* nbr, const int32_t* q,
+                                                      const unsigned long long* qn, const uint32_t* vis,
+                                                      uint32_t* disc, unsigned long long* scanned) {
   const int64_t n = (int64_t)*qn;
   const int lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -70,36 +73,40 @@ __global__ void __launch_bounds__(256) k_bfsd_push(const int64_t* off, const int
     cnt += e1 - e0;
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const int32_t v = __ldg(nbr + e);
-      if (!bit_of(vis, v)) atomicMax(cand + v, u);
+      const uint32_t m = 1u << (v & 31);
+      if (!(vis[v >> 5] & m) && !(*((volatile uint32_t*)disc + (v >> 5)) & m)) atomicOr(disc + (v >> 5), m);
     }
   }
   if (lane == 0 && cnt) atomicAdd(scanned, cnt);
 }
 
-// after the all-reduce(max): next = discovered (replicated), vis |= next,
-// owners take their parents, cand reset; frontier size by popcount
-__global__ void k_bfsd_push_commit(int32_t* cand, int32_t* parent, int64_t V, int64_t lo, int64_t hi,
-                                   uint32_t* vis, uint32_t* nx, unsigned long long* size) {
+// owner commit of a top-down level: the OR-ed discovered words of [w0, w1)
+// minus the visited ones are the next frontier; each new vertex takes its
+// first in-arc from the (replicated) frontier as parent
+__global__ void __launch_bounds__(256) k_bfsd_td_commit(const int64_t* in_off, const int32_t* in_nbr, int64_t w0,
+                                                        int64_t w1, const uint32_t* disc, const uint32_t* vis,
+                                                        const uint32_t* fr, int32_t* parent, uint32_t* nx) {
   const int lane = lane_id();
-  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); base < V;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = base + lane;
-    bool hit = false;
-    if (v < V) {
-      const int32_t c = cand[v];
-      if (c >= 0) {
-        hit = !bit_of(vis, v);
-        if (hit && v >= lo && v < hi) parent[v] = c;
-        cand[v] = -1;
+  for (int64_t w = w0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); w < w1;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint32_t fresh = disc[w] & ~vis[w];
+    if ((fresh >> lane) & 1u) {
+      const int64_t v = w * 32 + lane;
+      for (int64_t e = in_off[v], e1 = in_off[v + 1]; e < e1; ++e) {
+        const int32_t u = __ldg(in_nbr + e);
+        if (bit_of(fr, u)) {
+          parent[v] = u;
+          break;
+        }
       }
     }
-    const uint32_t word = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0) {
-      nx[base >> 5] = word;
-      vis[base >> 5] |= word;
-      if (word) atomicAdd(size, (unsigned long long)__popc(word));
-    }
+    if (lane == 0) nx[w] = fresh;
   }
+}
+
+__global__ void k_or_into(uint32_t* dst, const uint32_t* src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] |= src[i];
 }
 
 // bottom-up: thread per owned vertex; first in-arc from the frontier wins
@@ -158,17 +165,12 @@ __global__ void k_bfsd_bounds(const int64_t* off, int64_t V, int P, int64_t* bou
   bounds[r] = a & ~int64_t(31);
 }
 
-__global__ void k_max_into(int32_t* dst, const int32_t* src, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = max(dst[i], src[i]);
-}
-
 // one rank's state
 struct BfsRank {
   int dev = 0;
   int64_t V = 0, W = 0, lo = 0, hi = 0;
-  DevBuf<int32_t> parent, cand, q;
-  DevBuf<uint32_t> vis, fr, nx;
+  DevBuf<int32_t> parent, q;
+  DevBuf<uint32_t> vis, fr, nx, disc;  // disc: this rank's discovered bitmap of a top-down level
   DevBuf<unsigned long long> cnt;  // [0] queue length, [1] scanned arcs, [2] next frontier size
   int launches = 0;
   void alloc(int device, int64_t nv, int64_t l, int64_t h) {
@@ -178,11 +180,11 @@ struct BfsRank {
     lo = l;
     hi = h;
     parent.alloc(V);
-    cand.alloc(V);
     q.alloc(std::max<int64_t>(h - l, 1));
     vis.alloc(W);
     fr.alloc(W);
     nx.alloc(W);
+    disc.alloc(W);
     cnt.alloc(3);
   }
 };
@@ -210,14 +212,11 @@ int64_t bfs_dist_levels(const Graph& g, std::vector<BfsRank*>& rs, BfsExchange& 
   for (size_t i = 0; i < bounds.size(); ++i) wb[i] = (bounds[i] + 31) / 32;
   wb.back() = rs[0]->W;
   for (auto* R : rs) {
-    k_bfsd_init<<<grid_for(V, 256, dev), 256, 0, st>>>(R->parent.p, R->cand.p, V, R->vis.p, R->fr.p, R->nx.p, R->W,
-                                                       source);
+    k_bfsd_init<<<grid_for(V, 256, dev), 256, 0, st>>>(R->parent.p, V, R->vis.p, R->fr.p, R->nx.p, R->W, source);
     GG_LAUNCH_CHECK();
     ++R->launches;
   }
   int64_t size = 1, levels = 0, scanned = 0;
-  std::vector<int32_t*> cands;
-  for (auto* R : rs) cands.push_back(R->cand.p);
   while (size > 0) {
     const bool pull = (double)size > theta * (double)V;  // strictly greater (engine.py:632)
     rt.edge_begin();
@@ -225,8 +224,10 @@ int64_t bfs_dist_levels(const Graph& g, std::vector<BfsRank*>& rs, BfsExchange& 
       GG_CUDA(cudaMemsetAsync(R->cnt.p, 0, 3 * sizeof(unsigned long long), st));
       if (!pull) {
         const int64_t w0 = R->lo / 32, w1 = (R->hi + 31) / 32;
+        GG_CUDA(cudaMemsetAsync(R->disc.p, 0, R->W * sizeof(uint32_t), st));
         if (w1 > w0) k_bfsd_queue<<<grid_for(w1 - w0, 256, dev), 256, 0, st>>>(R->fr.p, w0, w1, R->q.p, R->cnt.p);
-        k_bfsd_push<<<grid, 256, 0, st>>>(out.off, out.nbr, R->q.p, R->cnt.p, R->vis.p, R->cand.p, R->cnt.p + 1);
+        k_bfsd_push_bm<<<grid, 256, 0, st>>>(out.off, out.nbr, R->q.p, R->cnt.p, R->vis.p, R->disc.p,
+                                             R->cnt.p + 1);
       } else {
         k_bfsd_pull<<<grid, 256, 0, st>>>(in.off, in.nbr, R->lo, R->hi, R->vis.p, R->fr.p, R->parent.p, R->nx.p,
                                           R->cnt.p + 1);
@@ -235,13 +236,22 @@ int64_t bfs_dist_levels(const Graph& g, std::vector<BfsRank*>& rs, BfsExchange& 
       R->launches += 2;
     }
     if (!pull) {
-      ex.allreduce_max_i32(cands, V, st);
-      for (auto* R : rs) {
-        k_bfsd_push_commit<<<grid_for(V, 256, dev), 256, 0, st>>>(R->cand.p, R->parent.p, V, R->lo, R->hi, R->vis.p,
-                                                                  R->nx.p, R->cnt.p + 2);
+      // discovered bits to their owners (OR), owners pick parents and form
+      // their words of the next frontier
+      std::vector<uint32_t*> discs;
+      for (auto* R : rs) discs.push_back(R->disc.p);
+      ex.alltoall_or_words(discs, wb, st);
+      for (size_t i = 0; i < rs.size(); ++i) {
+        BfsRank* R = rs[i];
+        const int64_t w0 = R->lo / 32, w1 = (R->hi + 31) / 32;
+        if (w1 > w0)
+          k_bfsd_td_commit<<<grid_for((w1 - w0) * 32, 256, dev), 256, 0, st>>>(in.off, in.nbr, w0, w1, R->disc.p,
+                                                                                R->vis.p, R->fr.p, R->parent.p,
+                                                                                R->nx.p);
         ++R->launches;
       }
-    } else {
+    }
+    {  // owned next-frontier words to every rank, then vis |= next
       std::vector<void*> nxs;
       for (auto* R : rs) nxs.push_back(R->nx.p);
       ex.allgather_bytes(nxs, sizeof(uint32_t), wb, st);
@@ -279,15 +289,20 @@ int64_t bfs_dist_levels(const Graph& g, std::vector<BfsRank*>& rs, BfsExchange& 
 }
 
 // Virtual ranks on one device (test mode of the multi-GPU path).
+// Byte accounting (both exchanges): bytes RANK 0 receives, the per-rank
+// exchange volume a real run moves (gg_bfs_exchange_bytes).
 struct BfsCopyExchange : BfsExchange {
   int dev;
   explicit BfsCopyExchange(int d) : dev(d) {}
-  void allreduce_max_i32(std::vector<int32_t*>& bufs, int64_t n, cudaStream_t st) override {
-    for (size_t i = 1; i < bufs.size(); ++i)
-      k_max_into<<<grid_for(n, 256, dev), 256, 0, st>>>(bufs[0], bufs[i], n);
+  void alltoall_or_words(std::vector<uint32_t*>& bufs, const std::vector<int64_t>& wb, cudaStream_t st) override {
+    const int P = (int)bufs.size();
+    for (int r = 0; r < P; ++r) {
+      const int64_t n = wb[r + 1] - wb[r];
+      for (int q = 0; q < P; ++q)
+        if (q != r && n > 0) k_or_into<<<grid_for(n, 256, dev), 256, 0, st>>>(bufs[r] + wb[r], bufs[q] + wb[r], n);
+    }
     GG_LAUNCH_CHECK();
-    for (size_t i = 1; i < bufs.size(); ++i)
-      GG_CUDA(cudaMemcpyAsync(bufs[i], bufs[0], n * 4, cudaMemcpyDeviceToDevice, st));
+    bytes += (uint64_t)(P - 1) * (uint64_t)(wb[1] - wb[0]) * 4;  // rank 0's slice from every peer
   }
   void allgather_bytes(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
                        cudaStream_t st) override {
@@ -297,6 +312,7 @@ struct BfsCopyExchange : BfsExchange {
         if (q != r && len)
           GG_CUDA(cudaMemcpyAsync((char*)bufs[q] + off, (char*)bufs[r] + off, len, cudaMemcpyDeviceToDevice, st));
     }
+    bytes += (uint64_t)(bounds.back() - bounds[0] - (bounds[1] - bounds[0])) * elt;  // all slices but its own
   }
 };
 
@@ -320,6 +336,7 @@ int64_t bfs_virtual(const Graph& g, int nparts, int64_t source, double theta, in
   }
   BfsCopyExchange ex(g.dev);
   int64_t levels = bfs_dist_levels(g, rp, ex, bounds, (int32_t)source, theta, st, rt, nullptr);
+  set_exchange_bytes(ex.bytes);
   GG_CUDA(cudaMemcpyAsync(parents_out, rs[0].parent.p, g.V * 4, cudaMemcpyDefault, st));
   GG_CUDA(cudaStreamSynchronize(st));
   int launches = 0;
@@ -337,6 +354,7 @@ int64_t bfs_rank(const Graph& g, int P, int r, BfsExchange& ex, int64_t source, 
   R.alloc(g.dev, g.V, bounds[r], bounds[r + 1]);
   std::vector<BfsRank*> rp{&R};
   int64_t levels = bfs_dist_levels(g, rp, ex, bounds, (int32_t)source, theta, st, rt, nullptr);
+  set_exchange_bytes(ex.bytes);
   GG_CUDA(cudaMemcpyAsync(parents_out, R.parent.p, g.V * 4, cudaMemcpyDefault, st));
   GG_CUDA(cudaStreamSynchronize(st));
   count_launch(R.launches);

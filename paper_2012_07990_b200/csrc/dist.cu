@@ -26,6 +26,8 @@ struct NcclApi {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
   ncclResult_t (*GroupStart)();
   ncclResult_t (*GroupEnd)();
   const char* (*GetErrorString)(ncclResult_t);
@@ -49,6 +51,8 @@ static NcclApi& nccl() {
   api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
   api.Broadcast = (decltype(api.Broadcast))sym("ncclBroadcast");
   api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+  api.Send = (decltype(api.Send))sym("ncclSend");
+  api.Recv = (decltype(api.Recv))sym("ncclRecv");
   api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
   api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
   api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
@@ -283,11 +287,38 @@ struct NcclExchange : PrExchange {
   }
 };
 
+__global__ void k_or_slices(uint32_t* dst, const uint32_t* stage, int64_t n, int parts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = dst[i];
+    for (int k = 0; k < parts; ++k) x |= stage[(int64_t)k * n + i];
+    dst[i] = x;
+  }
+}
+
 struct NcclBfsExchange : BfsExchange {
   gg_comm* c;
+  DevBuf<uint32_t> stage;  // the peers' slices of this rank's word range
   explicit NcclBfsExchange(gg_comm* cc) : c(cc) {}
-  void allreduce_max_i32(std::vector<int32_t*>& bufs, int64_t n, cudaStream_t st) override {
-    GG_NCCL(nccl().AllReduce(bufs[0], bufs[0], (size_t)n, ncclInt32, ncclMax, c->comm, st));
+  // grouped send/recv: my slice of every peer's bitmap arrives in `stage`,
+  // then one kernel ORs them into my words (V/8 bytes per rank per level)
+  void alltoall_or_words(std::vector<uint32_t*>& bufs, const std::vector<int64_t>& wb, cudaStream_t st) override {
+    NcclApi& api = nccl();
+    const int P = c->nranks, me = c->rank;
+    const int64_t mine = wb[me + 1] - wb[me];
+    if ((int64_t)stage.n < std::max<int64_t>(mine * (P - 1), 1)) stage.alloc(std::max<int64_t>(mine * (P - 1), 1));
+    GG_NCCL(api.GroupStart());
+    for (int q = 0, k = 0; q < P; ++q) {
+      if (q == me) continue;
+      const int64_t nq = wb[q + 1] - wb[q];
+      if (nq) GG_NCCL(api.Send(bufs[0] + wb[q], (size_t)nq, ncclUint32, q, c->comm, st));
+      if (mine) GG_NCCL(api.Recv(stage.p + (int64_t)k * mine, (size_t)mine, ncclUint32, q, c->comm, st));
+      ++k;
+    }
+    GG_NCCL(api.GroupEnd());
+    if (mine && P > 1)
+      k_or_slices<<<grid_for(mine, 256, c->dev), 256, 0, st>>>(bufs[0] + wb[me], stage.p, mine, P - 1);
+    GG_LAUNCH_CHECK();
+    bytes += (uint64_t)(P - 1) * (uint64_t)mine * 4;
   }
   void allgather_bytes(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
                        cudaStream_t st) override {
@@ -299,6 +330,7 @@ struct NcclBfsExchange : BfsExchange {
       if (cnt) GG_NCCL(api.Broadcast(p, p, cnt, ncclUint8, r, c->comm, st));
     }
     GG_NCCL(api.GroupEnd());
+    bytes += (uint64_t)(bounds.back() - bounds[0] - (bounds[c->rank + 1] - bounds[c->rank])) * elt;
   }
 };
 

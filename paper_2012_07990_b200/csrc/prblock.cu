@@ -116,6 +116,11 @@ __global__ void k_edge_keys(const int32_t* s, const int32_t* d, int64_t E, const
   }
 }
 template <class KT>
+__global__ void k_owned_flags(const KT* key, int64_t E, uint64_t K, int nvb, uint8_t* flags) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    flags[e] = ((uint64_t)key[e] >> nvb) < K;
+}
+template <class KT>
 __global__ void k_count_hot(const KT* key, int64_t E, int shift, unsigned long long* n) {
   unsigned long long c = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
@@ -178,21 +183,44 @@ static void sort_edges(const Graph& g, PrBlockLayout* L, int nvb, int kb, int64_
   const int dev = g.dev;
   const int64_t Eall = g.E;
   const int shift = nvb;
-  DevBuf<KT> keys(Eall);
+  DevBuf<KT> keys(std::max<int64_t>(E, 1));
   {
     DevBuf<KT> k0(Eall);
     DevBuf<int32_t> v0(Eall);
-    L->src.alloc(Eall);  // payload: renumbered sources in (segment, destination) order
     k_edge_keys<KT><<<grid_for(Eall, 256, dev), 256>>>(g.coo_src.p, g.coo_dst.p, Eall, L->newid.p, L->ns,
                                                        L->ns_cold, nvb,
                                                        L->lo, L->hi, (uint64_t)L->K, k0.p, v0.p);
     GG_LAUNCH_CHECK();
+    DevBuf<KT> k1;
+    DevBuf<int32_t> v1;
+    KT* kin = k0.p;
+    int32_t* vin = v0.p;
+    if (E < Eall) {
+      // a partitioned run keeps only the edges into its own destinations
+      // (order-preserving, so the stable sort's ties stay in COO order): the
+      // layout and the sort scale with the rank's E, not the graph's
+      k1.alloc(std::max<int64_t>(E, 1));
+      v1.alloc(std::max<int64_t>(E, 1));
+      DevBuf<uint8_t> flags(Eall);
+      DevBuf<unsigned long long> nsel(1);
+      k_owned_flags<KT><<<grid_for(Eall, 256, dev), 256>>>(k0.p, Eall, (uint64_t)L->K, nvb, flags.p);
+      GG_LAUNCH_CHECK();
+      size_t t1 = 0, t2 = 0;
+      GG_CUDA(cub::DeviceSelect::Flagged(nullptr, t1, k0.p, flags.p, k1.p, nsel.p, Eall));
+      GG_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, v0.p, flags.p, v1.p, nsel.p, Eall));
+      DevBuf<uint8_t> tb(std::max(t1, t2));
+      GG_CUDA(cub::DeviceSelect::Flagged(tb.p, t1, k0.p, flags.p, k1.p, nsel.p, Eall));
+      GG_CUDA(cub::DeviceSelect::Flagged(tb.p, t2, v0.p, flags.p, v1.p, nsel.p, Eall));
+      kin = k1.p;
+      vin = v1.p;
+    }
+    L->src.alloc(std::max<int64_t>(E, 1));  // payload: renumbered sources in (segment, destination) order
     size_t temp = 0;
-    GG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, k0.p, keys.p, v0.p, L->src.p, Eall, 0, nvb + kb));
-    DevBuf<uint8_t> tb(temp);
-    GG_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, temp, k0.p, keys.p, v0.p, L->src.p, Eall, 0, nvb + kb));
+    GG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, kin, keys.p, vin, L->src.p, E, 0, nvb + kb));
+    DevBuf<uint8_t> tb(std::max<size_t>(temp, 1));
+    GG_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, temp, kin, keys.p, vin, L->src.p, E, 0, nvb + kb));
   }
-  L->src.n = E;  // foreign edges (partitioned run) sort past E
+  L->src.n = E;
   L->dst.alloc(E);
   k_dst_of_keys<KT><<<grid_for(E, 256, dev), 256>>>(keys.p, E, nvb, L->dst.p);
   DevBuf<int64_t> se(L->K + 1);
@@ -514,9 +542,10 @@ __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, co
   }
 }
 
-template <class CT, bool kPrefetch>
-static __global__ void __launch_bounds__(256) k_pr_edges(const int32_t* src, const int32_t* dst, int64_t e0,
-                                                         int64_t e1, const CT* contrib, double* acc) {
+template <class CT, bool kPrefetch, int kMinBlocks = 1>
+static __global__ void __launch_bounds__(256, kMinBlocks) k_pr_edges(const int32_t* src, const int32_t* dst,
+                                                                     int64_t e0, int64_t e1, const CT* contrib,
+                                                                     double* acc) {
   pr_edges_seg<CT, false, kPrefetch>(src, dst, e0, e1, contrib, acc, 0);
 }
 
@@ -689,6 +718,7 @@ struct HotCfg {
   bool prefetch = true;
   int gather = 0;
   int32_t cold_from = INT32_MAX;  // one-segment layout: first source past the L2 window
+  int cold_minb = 0;              // cold-segment kernel register cap (GG_PR_COLD_MINB)
   unsigned grid = 0, hot_grid = 0;
 };
 
@@ -737,7 +767,13 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
     const void* fn = h.gather == 1 ? (const void*)k_pr_edges_hot<CT, 1024, 1, 1> : (const void*)k_pr_edges_hot<CT, 1024, 1, 2>;
     GG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, h.nhot * (int)sizeof(CT)));
   }
-  h.grid = (unsigned)sm_count(dev) * 8;
+  // cold segments: GG_PR_COLD_MINB = 6 / 8 caps registers for 6 / 8 resident
+  // CTAs per SM (default: the compiler's 64 registers, 4 per SM); the grid
+  // is GG_PR_COLD_GRID CTAs per SM (default 8)
+  if (const char* e = getenv("GG_PR_COLD_MINB")) h.cold_minb = atoi(e);
+  int per = 8;
+  if (const char* e = getenv("GG_PR_COLD_GRID")) per = std::max(1, atoi(e));
+  h.grid = (unsigned)sm_count(dev) * per;
   h.hot_grid = (unsigned)sm_count(dev) * h.per_sm;
   return h;
 }
@@ -820,7 +856,14 @@ struct PrRank {
         k_pr_edges_hot<CT, 1024, 1><<<hc.hot_grid, 1024, hc.nhot * sizeof(CT), st>>>(L->src.p, L->dst.p, e0, e1,
                                                                                     c, acc, hc.nhot);
       else if (hc.prefetch)
-        k_pr_edges<CT, true><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+      {
+        if (hc.cold_minb == 6)
+          k_pr_edges<CT, true, 6><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+        else if (hc.cold_minb == 8)
+          k_pr_edges<CT, true, 8><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+        else
+          k_pr_edges<CT, true><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
+      }
       else
         k_pr_edges<CT, false><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, e0, e1, c, acc);
       if (ta) {

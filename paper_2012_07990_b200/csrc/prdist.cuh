@@ -51,15 +51,22 @@ struct PrExchange {
 };
 
 // Exchange of the partitioned BFS (bfsdist.cu): an element-wise max of an
-// int32 array (top-down parent candidates) and an all-gather of owned slices
-// (bottom-up next-frontier words, final parents).
+// all-to-all of discovered-bitmap slices OR-ed at their owners (top-down) and
+// an all-gather of owned slices (next-frontier words, final parents).
 struct BfsExchange {
+  uint64_t bytes = 0;  // received by one rank over the run (exchange volume)
   virtual ~BfsExchange() {}
-  virtual void allreduce_max_i32(std::vector<int32_t*>& bufs, int64_t n, cudaStream_t st) = 0;
+  // top-down: every rank's V-bit discovered bitmap; the owner of word range
+  // [wb[r], wb[r+1]) ends with the OR over all ranks in its slice
+  virtual void alltoall_or_words(std::vector<uint32_t*>& bufs, const std::vector<int64_t>& wb,
+                                 cudaStream_t st) = 0;
   virtual void allgather_bytes(std::vector<void*>& bufs, size_t elt, const std::vector<int64_t>& bounds,
                                cudaStream_t st) = 0;
 };
 int64_t bfs_virtual(const Graph& g, int nparts, int64_t source, double theta, int32_t* parents_out, Runtime& rt);
+// bytes one rank received in the last partitioned / virtual run on this thread
+void set_exchange_bytes(uint64_t b);
+uint64_t last_exchange_bytes();
 int64_t bfs_rank(const Graph& g, int P, int r, BfsExchange& ex, int64_t source, double theta, int32_t* parents_out,
                  Runtime& rt);
 

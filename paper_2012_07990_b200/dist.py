@@ -171,6 +171,14 @@ def bfs_dist(comm, g, source, threshold=0.05, out=None):
     return parents, RunStats.from_pod(st)
 
 
+def last_exchange_bytes():
+    """Bytes one rank received through the exchange in the last bfs_dist /
+    bfs_virtual call on this thread (gg_last_exchange_bytes)."""
+    b = C.c_uint64(0)
+    _lib.call("gg_last_exchange_bytes", C.byref(b))
+    return int(b.value)
+
+
 def bfs_virtual(g, nparts, source, threshold=0.05, out=None):
     """The partitioned BFS with `nparts` virtual ranks on one device (test mode)."""
     if not 0 <= source < g.num_vertices:

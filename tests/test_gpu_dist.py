@@ -109,6 +109,33 @@ def test_bfs_virtual_ranks_levels_and_tree(nparts, theta):
             assert set(st.direction_log) == {"PUSH"}
 
 
+@pytest.mark.parametrize("nparts", [2, 4, 8])
+@pytest.mark.parametrize("theta", [1e-9, 0.999999])
+def test_bfs_virtual_exchange_is_bitmaps(nparts, theta):
+    """Per level one rank receives bitmap words only: top-down the owners'
+    slices of the peers' discovered bitmaps, then everyone else's words of the
+    next frontier -- at most 2 * V/8 bytes, never a V-long int32
+    array -- plus the final V*4-byte parent all-gather."""
+    import paper_2012_07990_b200 as gg
+    from paper_2012_07990_b200.dist import bfs_dist_bounds, bfs_virtual, last_exchange_bytes
+    g = gg.generate_rmat(12, 8, seed=5, symmetrize=True)
+    V = g.num_vertices
+    off, nbr, _ = oracle.csr(V, g.coo_src, g.coo_dst)
+    src = int(np.argmax(np.diff(off)))
+    parents, st = bfs_virtual(g, nparts, src, theta)
+    _levels_and_tree(gg, g, parents, src, off, nbr)
+    got = last_exchange_bytes()
+    b = [int(x) for x in bfs_dist_bounds(g, nparts)]
+    W = (V + 31) // 32
+    wb = [(x + 31) // 32 for x in b]
+    wb[-1] = W
+    own = wb[1] - wb[0]
+    parent_bytes = (V - (b[1] - b[0])) * 4
+    per_level = 4 * (W - own) + (4 * (nparts - 1) * own if theta > 0.5 else 0)
+    assert got == parent_bytes + st.rounds * per_level
+    assert per_level <= 2 * W * 4  # bitmap words, not 4 bytes per vertex
+
+
 def test_bfs_dist_single_rank_matches_oracle():
     import paper_2012_07990_b200 as gg
     from paper_2012_07990_b200.dist import Comm, bfs_dist
