@@ -303,13 +303,21 @@ int gg_pagerank_ex(const gg_graph* g, const gg_binding* binding, int32_t fusion,
                    int32_t fp32_contrib, double* ranks, gg_stats* stats);
 /* Locality relabelling for the frontier algorithms (no reference
  * counterpart; a layout choice like EdgeBlocking): gg_bc runs on a copy of
- * the graph renumbered by degree (descending, dealt over 1024 id ranges) when
+ * the graph renumbered by degree (descending) when
  * the graph has >= 2^20 vertices, gg_cc / gg_bfs only when GG_RELABEL=1
  * (GG_RELABEL=0 turns it off everywhere); results map back to the original
  * ids -- canonical CC labels stay each component's minimum original id.
  * This builds the copy ahead of the queries (cached on the graph) and
  * reports its preprocessing time. */
 int gg_relabel_prepare(const gg_graph* g, double* prep_ms);
+/* gg_pagerank continued from a given rank vector (host or device, original
+ * ids) instead of rank_0 = 1/n: the power iteration's whole state between
+ * iterations is the rank vector, so k calls of one iteration each equal one
+ * call of k.  pagerank(on_iteration=...) drives it one iteration per call
+ * (algos.py:163-208 observes every iteration). */
+int gg_pagerank_resume(const gg_graph* g, const gg_binding* binding, int32_t fusion,
+                       const gg_exec* cfg, int64_t max_iters, double tolerance, double damping,
+                       const double* init_ranks, double* ranks, gg_stats* stats);
 int gg_sssp_delta(const gg_graph* g, int64_t source, const gg_binding* binding,
                   int32_t fusion, const gg_exec* cfg, uint64_t* dist, gg_stats* stats); /* algos.py:215 */
 int gg_cc(const gg_graph* g, const gg_binding* binding, int32_t fusion, const gg_exec* cfg,

@@ -131,6 +131,8 @@ SIGNATURES = {
     "gg_last_exchange_bytes": (I32, [C.POINTER(C.c_uint64)]),
     "gg_pagerank_ex": (I32, [VP, C.POINTER(GGBinding), I32, C.POINTER(GGExec), I64, F64,
                              F64, I32, VP, C.POINTER(GGStats)]),
+    "gg_pagerank_resume": (I32, [VP, C.POINTER(GGBinding), I32, C.POINTER(GGExec), I64, F64,
+                                 F64, VP, VP, C.POINTER(GGStats)]),
     "gg_sssp_delta": (I32, [VP, I64, C.POINTER(GGBinding), I32, C.POINTER(GGExec), VP,
                             C.POINTER(GGStats)]),
     "gg_cc": (I32, [VP, C.POINTER(GGBinding), I32, C.POINTER(GGExec), VP,

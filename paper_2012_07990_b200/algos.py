@@ -187,21 +187,33 @@ def pagerank(g, program=None, exec_cfg=None, max_iters=100, tolerance=1e-9, damp
 
 
 def _pagerank_observed(g, plan, pod, cfg, max_iters, tolerance, damping, on_iteration):
-    # Observing every iteration: run k = 1..n iteration prefixes on the device.
-    # Deterministic per k, so the k-th call reproduces the k-th iterate.
-    st = _lib.new_stats()
-    ranks = np.empty(g.num_vertices, np.float64)
-    done = 0
-    prev = None
-    while done < max_iters:
-        _lib.call("gg_pagerank", g.handle, C.byref(pod), 1 if plan.fusion else 0,
-                  C.byref(cfg), done + 1, 0.0, float(damping), _lib.ptr(ranks), C.byref(st))
-        done += 1
+    # Observing every iteration: one device iteration per call, each resumed
+    # from the previous ranks (gg_pagerank_resume; the rank vector is the
+    # whole state between iterations), so n iterations cost n, not n(n+1)/2.
+    # Stop test before each body with L1 = inf initially (algos.py:178,
+    # :204-205; engine.py:659-661).
+    V = g.num_vertices
+    prev = np.full(V, 1.0 / V, np.float64)
+    ranks = np.empty(V, np.float64)
+    total = RunStats()
+    it, l1 = 0, math.inf
+    while not (it >= max_iters or l1 < tolerance):
+        st = _lib.new_stats()
+        _lib.call("gg_pagerank_resume", g.handle, C.byref(pod), 1 if plan.fusion else 0,
+                  C.byref(cfg), 1, 0.0, float(damping), _lib.ptr(prev), _lib.ptr(ranks), C.byref(st))
+        one = RunStats.from_pod(st)
+        for f in ("dispatch_count", "rounds", "edges_traversed", "frontier_conversions",
+                  "frontier_allocations", "reused_frontiers", "creation_passes", "kernel_ms",
+                  "wall_ms", "gpu_launches", "edge_ms", "edge_launches", "top_ms", "top_launches"):
+            setattr(total, f, getattr(total, f) + getattr(one, f))
+        total.direction_log += one.direction_log
+        it += 1
+        l1 = float(np.abs(ranks - prev).sum())
         on_iteration(ranks.tolist())
-        if prev is not None and float(np.abs(ranks - prev).sum()) < tolerance:
-            break
-        prev = ranks.copy()
-    return AlgoResult(ranks.tolist(), RunStats.from_pod(st), ranks)
+        prev, ranks = ranks, prev
+    if plan.fusion:
+        total.dispatch_count = 1  # the whole loop is one fused dispatch (runtime.py:194-209)
+    return AlgoResult(prev.tolist(), total, prev)
 
 
 # ---------------------------------------------------------------------------

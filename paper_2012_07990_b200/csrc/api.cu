@@ -38,7 +38,7 @@ int64_t l2_bytes(int dev) {
 
 void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
                   int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
-                  bool fp32_contrib);
+                  bool fp32_contrib, const double* init_ranks = nullptr);
 void bfs_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
              int32_t* parents_out);
 void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, Runtime& rt,
@@ -912,6 +912,25 @@ int gg_pagerank_prepare(const gg_graph* g, const gg_binding* binding, int32_t fp
   }
   GG_CUDA(cudaDeviceSynchronize());
   if (prep_ms) *prep_ms = now_ms() - t0;
+  GG_API_END
+}
+
+int gg_pagerank_resume(const gg_graph* g, const gg_binding* binding, int32_t fusion, const gg_exec* cfg,
+                       int64_t max_iters, double tolerance, double damping, const double* init_ranks,
+                       double* ranks, gg_stats* stats) {
+  GG_API_BEGIN
+  NEED(g);
+  NEED(binding);
+  NEED(init_ranks);
+  NEED(ranks);
+  DeviceGuard guard(g->g->dev);
+  Runtime rt(g->g.get(), cfg);
+  CallTimer t(g->g->dev);
+  const int64_t V = g->g->V;
+  DevBuf<double> init(std::max<int64_t>(V, 1));
+  if (V) GG_CUDA(cudaMemcpyAsync(init.p, init_ranks, V * 8, cudaMemcpyDefault, rt.stream));
+  pagerank_run(*g->g, *binding, fusion != 0, cfg, max_iters, tolerance, damping, ranks, rt, false, init.p);
+  t.finish(g->g->dev, rt, stats);
   GG_API_END
 }
 

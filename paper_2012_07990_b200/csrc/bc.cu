@@ -39,6 +39,12 @@ __global__ void k_bc_init_aos(BcState* st, int64_t V, int64_t s) {
     st[v] = x;
   }
 }
+__global__ void k_bits_set(const int32_t* ids, int64_t n, uint32_t* bm) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = ids[i];
+    atomicOr(bm + (v >> 5), 1u << (v & 31));
+  }
+}
 __global__ void k_bc_accumulate_aos(const BcState* st, double* score, int64_t V, int64_t s) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
        v += (int64_t)gridDim.x * blockDim.x)
@@ -111,6 +117,8 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
   bwd.s1.direction = GG_PUSH;
   bwd.s2 = bwd.s1;
   DevBuf<BcState> state(std::max<int64_t>(V, 1));  // depth, sigma, delta per vertex: one sector
+  const int64_t W = (V + 31) / 32;
+  DevBuf<uint32_t> vis(std::max<int64_t>(W, 1)), nxt(std::max<int64_t>(W, 1));  // level bitmaps
   DevBuf<int32_t> order(V + 1);
   DevBuf<double> score(V);
   DevBuf<unsigned long long> nsel(1);
@@ -118,6 +126,7 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
   for (int64_t si = 0; si < nsrc; ++si) {
     const int64_t s = sources[si];
     k_bc_init_aos<<<grid_for(V, 256, dev), 256, 0, st>>>(state.p, V, s);
+    GG_CUDA(cudaMemsetAsync(vis.p, 0, std::max<int64_t>(W, 1) * 4, st));
     GG_LAUNCH_CHECK();
     count_launch();
     int32_t s32 = (int32_t)s;
@@ -126,9 +135,15 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
     int32_t level = 0;
     int64_t pos = 0;
     while (frontier_size(&rt, frontier.get()) > 0) {
+      const int64_t lo = pos;
       pos += snapshot(rt, frontier.get(), order.p, pos, nsel);
       level_start.push_back(pos);
-      OpBcFwdAoS op{state.p, level};
+      if (pos > lo) {  // this level joins the visited bitmap before its arcs are walked
+        k_bits_set<<<grid_for(pos - lo, 256, dev), 256, 0, st>>>(order.p + lo, pos - lo, vis.p);
+        GG_LAUNCH_CHECK();
+        count_launch();
+      }
+      OpBcFwdAoS op{state.p, level, vis.p};
       rt.edge_begin();
       std::unique_ptr<Frontier> out = apply_op(&rt, op, true, &frontier, b, true, true);
       rt.edge_end();
@@ -138,9 +153,16 @@ void bc_run(const Graph& g, const int64_t* sources, int64_t nsrc, const gg_bindi
     }
     rt.release(std::move(frontier));
     const int64_t nrounds = (int64_t)level_start.size() - 1;
-    OpBcBwdAoS bop{state.p};
+    OpBcBwdAoS bop{state.p, nxt.p};
     for (int64_t r = nrounds - 2; r >= 0; --r) {
       const int64_t lo = level_start[r], cnt = level_start[r + 1] - lo;
+      {  // bitmap of level r + 1
+        const int64_t l1 = level_start[r + 1], n1 = level_start[r + 2] - l1;
+        GG_CUDA(cudaMemsetAsync(nxt.p, 0, std::max<int64_t>(W, 1) * 4, st));
+        if (n1 > 0) k_bits_set<<<grid_for(n1, 256, dev), 256, 0, st>>>(order.p + l1, n1, nxt.p);
+        GG_LAUNCH_CHECK();
+        count_launch();
+      }
       std::unique_ptr<Frontier> wave = rt.acquire(GG_SPARSE);  // new_frontier(n, rounds[r])
       GG_CUDA(cudaMemcpyAsync(wave->ids.p, order.p + lo, cnt * 4, cudaMemcpyDeviceToDevice, st));
       unsigned long long c = (unsigned long long)cnt;

@@ -266,12 +266,20 @@ struct __align__(32) BcState {
   int32_t depth;
   int32_t pad[3];
 };
+// `vis`: bitmap of the vertices of levels 0..level (set between rounds); an
+// arc into one of them is dropped with an L2-resident bit test instead of a
+// random 32-byte state gather (the frontier's arcs mostly lead back).
+__device__ __forceinline__ bool bm_has(const uint32_t* bm, int32_t v) {
+  return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
+}
 struct OpBcFwdAoS {
   BcState* st;
   int32_t level;
+  const uint32_t* vis;
   using Acc = BcAcc;
   static constexpr bool kEarlyExit = false;
   __device__ __forceinline__ bool filter(int32_t v) const {
+    if (bm_has(vis, v)) return false;  // depth <= level: neither -1 nor level + 1
     const int32_t d = *((volatile int32_t*)&st[v].depth);
     return d == -1 || d == level + 1;
   }
@@ -297,12 +305,16 @@ struct OpBcFwdAoS {
     st[v].sigma += a.s;
   }
 };
+// `next`: bitmap of the level after the frontier's; only arcs into it carry
+// a dependency (depth[v] == depth[u] + 1), the rest skip the state gather.
 struct OpBcBwdAoS {
   BcState* st;
+  const uint32_t* next;
   using Acc = int;
   static constexpr bool kEarlyExit = false;
   __device__ __forceinline__ bool filter(int32_t) const { return true; }
   __device__ __forceinline__ double contrib(int32_t u, int32_t v) const {
+    if (!bm_has(next, v)) return 0.0;
     // one 32-byte load of v's state (depth, sigma, delta); u's is per range
     const double2 sd = __ldg(reinterpret_cast<const double2*>(&st[v]));  // v's state is final
     const int32_t dv = __ldg(&st[v].depth);                               // (same sector: L1 hit)

@@ -20,14 +20,16 @@
 
 namespace gg {
 
+// rank_0 = 1/n (algos.py:178), or the given vector (a resumed power
+// iteration: gg_pagerank_resume, the observed loop of pagerank(on_iteration))
 template <class CT>
 __global__ void __launch_bounds__(256) k_pr_init(const int64_t* off, int64_t V, double* rank,
-                                                 CT* contrib, double* acc, double* dm0) {
-  const double r0 = 1.0 / (double)V;
+                                                 CT* contrib, double* acc, double* dm0, const double* init) {
   double dm = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
        v += (int64_t)gridDim.x * blockDim.x) {
     int64_t d = off[v + 1] - off[v];
+    const double r0 = init ? init[v] : 1.0 / (double)V;
     rank[v] = r0;
     acc[v] = 0.0;
     contrib[v] = d ? (CT)(r0 / (double)d) : (CT)0;
@@ -365,7 +367,7 @@ static int64_t pagerank_pull_tiles(const Graph& g, bool fusion, int64_t max_iter
 template <class CT>
 static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
                           int64_t max_iters, double tol, double damping, double* ranks_out,
-                          Runtime& rt) {
+                          Runtime& rt, const double* init) {
   const int64_t V = g.V;
   const int dev = g.dev;
   cudaStream_t st = rt.stream;
@@ -374,7 +376,7 @@ static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, cons
   DevBuf<double> rank(V), acc(V), scal(2 * (iters_cap + 2));
   DevBuf<CT> contrib(V);
   scal.zero(st);
-  k_pr_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(g.out_off.p, V, rank.p, contrib.p, acc.p, scal.p);
+  k_pr_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(g.out_off.p, V, rank.p, contrib.p, acc.p, scal.p, init);
   GG_LAUNCH_CHECK();
   count_launch();
   const gg_schedule& s = b.s1;
@@ -452,11 +454,12 @@ static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, cons
 
 template <class CT>
 int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int64_t max_iters,
-                         double tol, double damping, double* ranks_out, Runtime& rt);
+                         double tol, double damping, double* ranks_out, Runtime& rt,
+                         const double* init = nullptr);
 
 void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exec* cfg,
                   int64_t max_iters, double tol, double damping, double* ranks_out, Runtime& rt,
-                  bool fp32_contrib) {
+                  bool fp32_contrib, const double* init_ranks) {
   if (g.V == 0) fail(GG_ERR_VALUE, "empty graph");
   if (b.is_hybrid)
     fail(GG_ERR_SCHEDULE, "label 's0:s1' of pagerank takes a SimpleGPUSchedule (hybrid direction "
@@ -465,15 +468,15 @@ void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exe
   DeviceGuard guard(g.dev);
   if (b.s1.load_balance == GG_LB_EDGE_ONLY && b.s1.blocking) {
     if (fp32_contrib)
-      pagerank_blocked<float>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt);
+      pagerank_blocked<float>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt, init_ranks);
     else
-      pagerank_blocked<double>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt);
+      pagerank_blocked<double>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt, init_ranks);
     return;
   }
   if (fp32_contrib)
-    pagerank_impl<float>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt);
+    pagerank_impl<float>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt, init_ranks);
   else
-    pagerank_impl<double>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt);
+    pagerank_impl<double>(g, b, fusion, cfg, max_iters, tol, damping, ranks_out, rt, init_ranks);
 }
 
 }  // namespace gg

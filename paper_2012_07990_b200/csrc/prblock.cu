@@ -346,13 +346,15 @@ double pr_block_prep_ms(const Graph& g, int64_t blocking_size, int ct_bytes) {
   return layout_for(g, pr_block_window(g, ct_bytes, blocking_size), ct_bytes)->prep_ms;
 }
 
+// rank_0 = 1/n, or a given vector in original ids (order: renumbered -> original)
 template <class CT>
 static __global__ void __launch_bounds__(256) k_prb_init(const int32_t* outdeg, int64_t V, double* rank,
-                                                         CT* contrib, double* dm0) {
-  const double r0 = 1.0 / (double)V;
+                                                         CT* contrib, double* dm0, const double* init,
+                                                         const int32_t* order) {
   double dm = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
        v += (int64_t)gridDim.x * blockDim.x) {
+    const double r0 = init ? init[order[v]] : 1.0 / (double)V;
     int32_t d = outdeg[v];
     rank[v] = r0;
     contrib[v] = d ? (CT)(r0 / (double)d) : (CT)0;
@@ -811,10 +813,10 @@ struct PrRank {
   }
   // rank_0 = 1/n, contrib_0, dangling mass_0 over ALL vertices (identical on
   // every rank, so no exchange precedes the first iteration)
-  void init(int64_t iters_cap, cudaStream_t st) {
+  void init(int64_t iters_cap, cudaStream_t st, const double* init_ranks = nullptr) {
     GG_CUDA(cudaMemsetAsync(scal, 0, 2 * (iters_cap + 2) * sizeof(double), st));
     GG_CUDA(cudaMemsetAsync(acc, 0, std::max<int64_t>(L->vloc(), 1) * sizeof(double), st));
-    k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank, c0, scal);
+    k_prb_init<CT><<<grid_for(V, 256, dev), 256, 0, st>>>(L->outdeg.p, V, rank, c0, scal, init_ranks, L->order.p);
     GG_LAUNCH_CHECK();
     ++launches;
   }
@@ -905,7 +907,7 @@ struct PrRank {
 
 template <class CT>
 int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int64_t max_iters,
-                         double tol, double damping, double* ranks_out, Runtime& rt) {
+                         double tol, double damping, double* ranks_out, Runtime& rt, const double* init) {
   const int dev = g.dev;
   const int64_t V = g.V;
   cudaStream_t st = rt.stream;
@@ -917,7 +919,7 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   PrRank<CT> R;
   R.bind(L, dev, iters_cap);
   R.rt_top = &rt;
-  R.init(iters_cap, st);
+  R.init(iters_cap, st, init);
   int64_t it = 0;
   if (!fusion) {
     double l1 = INFINITY;
@@ -968,9 +970,9 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
 }
 
 template int64_t pagerank_blocked<double>(const Graph&, const gg_schedule&, bool, int64_t, double,
-                                          double, double*, Runtime&);
+                                          double, double*, Runtime&, const double*);
 template int64_t pagerank_blocked<float>(const Graph&, const gg_schedule&, bool, int64_t, double,
-                                         double, double*, Runtime&);
+                                         double, double*, Runtime&, const double*);
 
 // ---------------------------------------------------------------------------
 // Partitioned (multi-rank) run.  Per iteration: local edge phase over the

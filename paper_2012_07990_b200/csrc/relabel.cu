@@ -2,8 +2,9 @@
 // (CC, BC, BFS): the same graph with vertices renumbered by degree,
 // descending (stable), cached on the Graph like the PageRank layout.
 //
-// The ranks are dealt over 1024 id ranges (rl_dealt below) rather than
-// numbered densely, so the hottest vertices do not share cache lines.
+// GG_RELABEL_DEAL=P deals the ranks over P id ranges (rl_dealt below)
+// instead of numbering them densely, so the hottest vertices do not share
+// cache lines (measured for CC; BC, the default user, is best dense).
 //
 // Why: Graph500 Kronecker inputs permute vertex ids, so the per-vertex state
 // those algorithms gather per arc (label[dst] in the CC hook, depth / sigma /
@@ -96,7 +97,7 @@ static std::shared_ptr<Relabel> build_relabel(const Graph& g) {
     GG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, key.p, key2.p, ids.p, by_rank.p, V));
     DevBuf<uint8_t> tb(std::max<size_t>(temp, 1));
     GG_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, temp, key.p, key2.p, ids.p, by_rank.p, V));
-    int64_t P = 1024;
+    int64_t P = 1;  // dense degree order (BC: 44.9 GTEPS hybrid vs 31.4 dealt over 1024 ranges)
     if (const char* e = getenv("GG_RELABEL_DEAL")) P = std::max<int64_t>(1, atoll(e));
     if (P > V) P = std::max<int64_t>(V, 1);
     R->deal = P;
@@ -137,8 +138,10 @@ const Graph* relabel_graph(const Relabel& R) { return R.g.get(); }
 double relabel_prep_ms(const Relabel& R) { return R.prep_ms; }
 
 // Policy: GG_RELABEL=0 / 1 forces it; by default only BC relabels (graphs
-// of >= 2^20 vertices).  Measured on Kronecker-25 / RMAT-24:
-// BC ETWC 11.1 -> 19.0 GTEPS, TWC 16.7 -> 20.9, hybrid 26.6 -> 33.3; CC loses
+// of >= 2^20 vertices).  Measured on Kronecker-25 / RMAT-24,
+// with the level-bitmap filters: BC ETWC 22.3 -> 29.8 GTEPS, TWC 24.0 -> 34.6,
+// hybrid 30.9 -> 44.9 (dense order; dealt over 1024 ranges: 22.9 / 25.2 /
+// 31.4); CC loses
 // (ETWC 121 -> 31..63: the hubs' adjacency lists cluster into a few CTAs of
 // the vertex-partitioned balancers, and dense numbering makes the hub labels'
 // L2 slices the bound), DO-BFS on RMAT-24 (natural ids already hub-first)

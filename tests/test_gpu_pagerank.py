@@ -112,6 +112,28 @@ def test_pagerank_mass_conserved_each_iteration(gg):
     assert all(abs(x - 1.0) <= 1e-12 for x in sums)
 
 
+@pytest.mark.parametrize("blocked", [False, True])
+def test_pagerank_observed_equals_plain_run(gg, blocked):
+    """pagerank(on_iteration=...) resumes one device iteration per call
+    (gg_pagerank_resume): the callback sees every iterate, the stop test runs
+    before each body with L1 = inf at first (algos.py:178, :204-205), and the
+    result equals the unobserved run -- at linear, not quadratic, cost."""
+    V, s, d = gen.rmat(10, 8, seed=9)
+    g = gg.Graph.from_coo(V, s, d)
+    prog = program_with(gg.Schedule(load_balance="EDGE_ONLY", blocking=blocked))
+    plain = gg.pagerank(g, prog, max_iters=60, tolerance=1e-7)
+    seen = []
+    obs = gg.pagerank(g, prog, max_iters=60, tolerance=1e-7, on_iteration=lambda r: seen.append(list(r)))
+    assert len(seen) == plain.stats.rounds == obs.stats.rounds
+    assert max_rel_err(obs.values, plain.values) < 1e-12
+    assert seen[-1] == obs.values
+    want, iters = oracle.pagerank(V, s, d, 60, 1e-7)
+    assert iters == len(seen)
+    assert max_rel_err(seen[-1], want) < PR_TOL
+    # every iterate conserves the mass
+    assert all(abs(sum(r) - 1.0) < 1e-9 for r in seen)
+
+
 def test_pagerank_errors(gg):
     g = gg.Graph.from_coo(2, [0], [1])
     with pytest.raises(gg.ScheduleError, match="hybrid"):

@@ -1,36 +1,56 @@
-"""Summarise an ncu report: key throughput/latency metrics and warp stall reasons."""
-import csv, subprocess, sys, io
+"""Summarise ncu --set full reports (one kernel each) into a text table:
+duration, DRAM bytes, throughputs, hit rates, occupancy, top stall reasons.
+python tools/ncu_summary.py OUT.txt REPORT.ncu-rep [...]"""
+import csv
+import io
+import subprocess
+import sys
 
-KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
-        "l1tex__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__thread_inst_executed_per_inst_executed.ratio", "launch__registers_per_thread",
-        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
-        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
-        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
-        "l1tex__throughput.avg.pct_of_peak_sustained_active", "launch__grid_size", "launch__block_size",
-        "smsp__cycles_active.avg", "sm__cycles_elapsed.avg"]
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1TEX % peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "LTS % peak"),
+    ("l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed", "L1->XBAR req % peak"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads / instruction"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("launch__registers_per_thread", "registers"),
+]
 
-def main(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units = rows[0], rows[1]
-    for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")]
-        print("==", name[:100])
-        for k in KEYS:
-            if k in hdr:
-                print("  %-60s %s %s" % (k, r[hdr.index(k)], units[hdr.index(k)]))
-        stalls = []
-        for i, k in enumerate(hdr):
-            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
-                try:
-                    stalls.append((float(r[i].replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
-                except ValueError:
-                    pass
-        tot = sum(s for s, _ in stalls) or 1
-        print("  stalls:", ", ".join("%s %.0f%%" % (n, 100 * s / tot) for s, n in sorted(stalls, reverse=True)[:6]))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+
+
+def stalls(d):
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    items = [(k[len(pre):], float(v[0].replace(",", ""))) for k, v in d.items()
+             if k.startswith(pre) and not k.endswith("_not_issued") and v[0]]
+    tot = sum(x for _, x in items) or 1.0
+    items.sort(key=lambda t: -t[1])
+    return ", ".join("%s %.0f%%" % (n, 100 * x / tot) for n, x in items[:5])
+
+
+def main():
+    out = open(sys.argv[1], "w")
+    for rep in sys.argv[2:]:
+        d = raw(rep)
+        out.write("## %s\n  kernel: %s\n" % (rep.split("/")[-1], d.get("Kernel Name", ("?",))[0]))
+        for k, name in KEYS:
+            if k in d:
+                out.write("  %-24s %s %s\n" % (name, d[k][0], d[k][1]))
+        out.write("  stalls (pc sampling): %s\n\n" % stalls(d))
+    out.close()
+
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        main(p)
+    main()
