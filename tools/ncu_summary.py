@@ -7,6 +7,7 @@ import subprocess
 import sys
 
 KEYS = [
+    ("launches in report", "launches in report (longest shown)"),
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "dram read"),
     ("dram__bytes_write.sum", "dram write"),
@@ -27,8 +28,13 @@ KEYS = [
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+    hdr, units = rows[0], rows[1]
+    # several launches in one report: the longest one
+    k = hdr.index("gpu__time_duration.sum")
+    vals = max(rows[2:], key=lambda r: float(r[k].replace(",", "") or 0))
+    d = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
+    d["launches in report"] = (str(len(rows) - 2), "")
+    return d
 
 
 def stalls(d):
