@@ -171,6 +171,23 @@ def rel_err(got, want):
     return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
 
 
+def _committed_traffic(kernel):
+    """DRAM bytes per launch of the C5 dominant kernel from the committed
+    ncu --set full capture (profiles/*/ncu_c5_top_kernel.json), used only
+    when the capture is of the kernel this run timed."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    for rnd in ("r02", "r01"):
+        path = os.path.join(here, "profiles", rnd, "ncu_c5_top_kernel.json")
+        if os.path.exists(path):
+            with open(path) as fh:
+                cap = json.load(fh)
+            if cap.get("kernel") == kernel:
+                return (cap["dram_bytes_read"] + cap["dram_bytes_write"],
+                        "dram__bytes_read.sum + dram__bytes_write.sum per launch, %s (%s)"
+                        % (os.path.relpath(path, here), cap.get("source", "")))
+    return None, "no committed ncu capture of %s" % kernel
+
+
 def reference_arm(args, metric, scale, ef, seed, iters, workload):
     """--impl reference: the oracle port of the reference's PageRank on the
     host cores, on THIS arm's graph (RMAT-27, generated on the host by the
@@ -363,10 +380,7 @@ def main():
     traffic, traffic_note = None, "no ncu capture committed for this configuration"
     if (top_n and args.schedule == "eb" and not args.fp32_contrib and scale == 27
             and world == 1 and not args.permute):
-        traffic = 16.291855e9 + 0.618621e9
-        traffic_note = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, "
-                        "profiles/r01/ncu_full_k_pr_edges_hot_f64.txt (= the streamed "
-                        "edges; the gathers hit L2)")
+        traffic, traffic_note = _committed_traffic(kernel.split(" ")[0])
 
     line = {"metric": metric, "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
