@@ -75,6 +75,7 @@ def parse():
                    help="c2: s1 with MONOTONIC_COUNTERS dedup (default off: the BFS CAS "
                         "already admits each vertex once, so the frontier is identical)")
     p.add_argument("--pull-lb", default="VERTEX_BASED", help="c2 pull-side load balance")
+    p.add_argument("--push-creation", default="FUSED", help="c2 push-side frontier creation")
     p.add_argument("--fusion", action="store_true", help="c1/c2/c5: fused loop (s0 kernel fusion)")
     p.add_argument("--side", type=int, default=None, help="c3 grid side")
     p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")

@@ -231,7 +231,8 @@ def bfs_c2(gg, args, peak):
     theta = args.theta
     hy = gg.HybridSchedule(threshold=theta,
                            s1=gg.Schedule(direction="PUSH", load_balance="ETWC",
-                                          dedup=args.dedup),
+                                          dedup=args.dedup,
+                                          frontier_creation=args.push_creation),
                            s2=gg.Schedule(direction="PULL", pull_frontier_repr="BITMAP",
                                           frontier_creation="UNFUSED_BITMAP",
                                           load_balance=args.pull_lb))
@@ -329,7 +330,7 @@ def sssp_c3(gg, args, peak):
     g = gg.generate_grid(side, seed=4, weights=True)
     gen_s = time.perf_counter() - t0
     V, A = g.num_vertices, g.num_edges
-    deltas = [args.delta] if args.delta else [4096, 8192, 16384]
+    deltas = [args.delta] if args.delta else [8192, 10240, 12288, 16384]
     dist = torch.empty(V, dtype=torch.int64, device="cuda")
 
     def program(d):

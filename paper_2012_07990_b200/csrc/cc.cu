@@ -30,6 +30,33 @@ __global__ void k_pointer_jump(int32_t* label, int64_t V, int* moved) {
   if (__any_sync(0xffffffffu, any) && lane_id() == 0 && !*((volatile int*)moved)) *moved = 1;
 }
 
+// the highest-degree vertex (its component is the giant one on the power-law
+// inputs): packed (degree, -id) max
+__global__ void k_argmax_degree(const int64_t* off, int64_t V, unsigned long long* best) {
+  unsigned long long m = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+    const unsigned long long key = (d << 32) | (unsigned long long)(0xffffffffu - (uint32_t)v);
+    if (key > m) m = key;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+    if (x > m) m = x;
+  }
+  if (lane_id() == 0 && m) atomicMax(best, m);
+}
+// giant bitmap: label[v] == label[hub] (after pointer jumping: a root label)
+__global__ void k_giant_bits(const int32_t* label, int64_t V, const unsigned long long* best, uint32_t* bits) {
+  const int32_t hub = (int32_t)(0xffffffffu - (uint32_t)(*best & 0xffffffffu));
+  const int32_t g = label[hub];
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31); base < V;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + lane_id();
+    const unsigned w = __ballot_sync(0xffffffffu, v < V && label[v] == g);
+    if (lane_id() == 0) bits[base >> 5] = w;
+  }
+}
+
 // first member (minimum id) of every label class, then relabel
 __global__ void k_cc_first(const int32_t* label, int64_t V, int32_t* first) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V;
@@ -74,6 +101,20 @@ void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32
     cc_fused(rt, b.s1, label.p, flags.p);
   } else {
     OpHook op{label.p, flags.p};
+    // giant-component filter (OpHook::giant), rebuilt after every round's
+    // pointer jumping; none before the first round (labels are the ids)
+    const int64_t W = (V + 31) / 32;
+    DevBuf<uint32_t> giant(std::max<int64_t>(W, 1));
+    DevBuf<unsigned long long> best(1);
+    const char* ng = getenv("GG_CC_NO_GIANT");
+    const bool use_giant = V > 0 && !(ng && atoi(ng) != 0);
+    if (use_giant) {
+      g.ensure_out();
+      best.zero(st);
+      k_argmax_degree<<<grid_for(V, 256, dev), 256, 0, st>>>(g.out_off.p, V, best.p);
+      GG_LAUNCH_CHECK();
+      count_launch();
+    }
     int h[2] = {1, 0};
     while (h[0]) {
       GG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int), st));
@@ -89,6 +130,12 @@ void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32
         GG_CUDA(cudaStreamSynchronize(st));
       } while (h[1]);
       rt.stats.rounds += 1;
+      if (use_giant && h[0]) {
+        k_giant_bits<<<grid_for(V, 256, dev), 256, 0, st>>>(label.p, V, best.p, giant.p);
+        GG_LAUNCH_CHECK();
+        count_launch();
+        op.giant = giant.p;
+      }
     }
   }
   GG_CUDA(cudaMemsetAsync(first.p, 0x7f, V * sizeof(int32_t), st));

@@ -119,10 +119,16 @@ struct OpPr {
 struct OpHook {
   int32_t* label;
   int* changed;
+  // optional (cc_run): bit v set iff label[v] was the giant component's root
+  // label when the round started; an arc between two such vertices joins
+  // one tree to itself, so its two random label reads are skipped (an
+  // L2-resident bit test instead: most arcs after the first round)
+  const uint32_t* giant = nullptr;
   using Acc = int;
   static constexpr bool kEarlyExit = false;
   __device__ __forceinline__ bool filter(int32_t) const { return true; }
   __device__ __forceinline__ void hook(int32_t u, int32_t v) const {
+    if (giant && ((__ldg(giant + (u >> 5)) >> (u & 31)) & (__ldg(giant + (v >> 5)) >> (v & 31)) & 1u)) return;
     int32_t la = *((volatile int32_t*)label + u), lb = *((volatile int32_t*)label + v);
     if (la == lb) return;
     int32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
