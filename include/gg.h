@@ -74,8 +74,11 @@ typedef struct {
 /* Shape of the CTA hierarchy (runtime.ExecConfig, runtime.py:26-50).
  * On the device cta_size is the block size used by the CTA-granular
  * load balancers (ETWC stage-2 chunk, TWC CTA threshold); warp_size must be
- * 32 there.  num_workers/deterministic are host-simulation knobs of the
- * reference and only validated here. */
+ * 32 there.  num_workers is a host-simulation knob of the reference and
+ * only validated here; deterministic = 1 makes gg_pagerank sum in the
+ * reference's fixed order (per destination in COO order, dangling mass and
+ * L1 in vertex order, no FMA): ranks bitwise equal to the reference's for
+ * EDGE_ONLY (+ BLOCKED) and PULL schedules (a slow correctness mode). */
 typedef struct {
   int32_t num_workers;
   int32_t cta_size;

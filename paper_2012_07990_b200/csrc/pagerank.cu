@@ -452,6 +452,99 @@ static void pagerank_impl(const Graph& g, const gg_binding& b, bool fusion, cons
   GG_CUDA(cudaStreamSynchronize(st));
 }
 
+// ---------------------------------------------------------------------------
+// ExecConfig(deterministic=True) (runtime.py:26-50, :167): the reference then
+// runs every dispatch inline in worker order, so PageRank's floating-point
+// sums follow one fixed order.  Here the same operations in the same order:
+// acc[d] summed from 0.0 over d's in-arcs in COO order (the CSR-in is a stable
+// sort of the COO by destination: the order the reference's EDGE_ONLY
+// apply -- blocked or not, blocking.py:78-113 is stable -- and its PULL
+// apply visit them); the dangling mass and the L1 summed sequentially in
+// vertex order (algos.py:184-198); every multiply, divide and add rounded
+// separately (__d*_rn: no FMA contraction, which the compiler would
+// otherwise apply to base + damping * acc).  The ranks are then bitwise equal
+// to the reference's for EDGE_ONLY (+ BLOCKED) and PULL schedules; PUSH
+// schedules, whose reference order follows the load balancer's source
+// order, get the same reproducible COO-order sums.  One thread carries each
+// sequential sum: a correctness mode, not a fast one.
+// ---------------------------------------------------------------------------
+__global__ void k_prd_contrib(const int64_t* out_off, int64_t V, const double* rank, double* contrib) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = out_off[v + 1] - out_off[v];
+    contrib[v] = d ? __ddiv_rn(rank[v], (double)d) : 0.0;  // rank[v] / d (algos.py:186-188)
+  }
+}
+// the dangling mass, sequentially in vertex order (algos.py:184-185)
+__global__ void k_prd_dangling(const int64_t* out_off, int64_t V, const double* rank, double* dm) {
+  double m = 0.0;
+  for (int64_t v = 0; v < V; ++v)
+    if (out_off[v + 1] == out_off[v]) m = __dadd_rn(m, rank[v]);
+  *dm = m;
+}
+// acc[d] in COO order: thread per destination walks its in-arcs in order
+__global__ void k_prd_acc(const int64_t* in_off, const int32_t* in_nbr, int64_t V, const double* contrib,
+                          double* acc) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < V; d += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int64_t e = in_off[d], e1 = in_off[d + 1]; e < e1; ++e) a = __dadd_rn(a, contrib[in_nbr[e]]);
+    acc[d] = a;
+  }
+}
+// rank' = base + damping * acc (algos.py:189-196), L1 sequentially in vertex order
+__global__ void k_prd_update(int64_t V, const double* acc, double* rank, double* nv_tmp, const double* dm,
+                             double damping) {
+  const double n = (double)V;
+  const double base = __dadd_rn(__ddiv_rn(__dsub_rn(1.0, damping), n), __ddiv_rn(__dmul_rn(damping, *dm), n));
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    nv_tmp[v] = __dadd_rn(base, __dmul_rn(damping, acc[v]));
+}
+__global__ void k_prd_l1(int64_t V, const double* nv, const double* rank, double* l1) {
+  double s = 0.0;
+  for (int64_t v = 0; v < V; ++v) s = __dadd_rn(s, fabs(__dsub_rn(nv[v], rank[v])));
+  *l1 = s;
+}
+
+static void pagerank_deterministic(const Graph& g, const gg_binding& b, int64_t max_iters, double tol,
+                                   double damping, double* ranks_out, Runtime& rt, const double* init) {
+  const int64_t V = g.V;
+  const int dev = g.dev;
+  cudaStream_t st = rt.stream;
+  CsrView out = g.out_view();
+  CsrView in = g.in_view();
+  DevBuf<double> rank(V), nv(V), contrib(V), acc(V), sc(2);
+  if (init) {
+    GG_CUDA(cudaMemcpyAsync(rank.p, init, V * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    std::vector<double> r0(V, 1.0 / (double)V);  // [1.0 / n] * n (algos.py:176)
+    GG_CUDA(cudaMemcpyAsync(rank.p, r0.data(), V * 8, cudaMemcpyHostToDevice, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+  }
+  const unsigned grid = grid_for(V, 256, dev);
+  int64_t it = 0;
+  double l1 = INFINITY;
+  while (!(it >= max_iters || l1 < tol)) {  // stop test before each body (engine.py:659-661)
+    k_prd_dangling<<<1, 1, 0, st>>>(out.off, V, rank.p, sc.p);
+    k_prd_contrib<<<grid, 256, 0, st>>>(out.off, V, rank.p, contrib.p);
+    rt.edge_begin();
+    k_prd_acc<<<grid, 256, 0, st>>>(in.off, in.nbr, V, contrib.p, acc.p);
+    rt.edge_end();
+    k_prd_update<<<grid, 256, 0, st>>>(V, acc.p, rank.p, nv.p, sc.p, damping);
+    k_prd_l1<<<1, 1, 0, st>>>(V, nv.p, rank.p, sc.p + 1);
+    GG_LAUNCH_CHECK();
+    count_launch(5);
+    std::swap(rank, nv);
+    ++it;
+    rt.stats.rounds += 1;
+    rt.stats.dispatch_count += 1;
+    rt.stats.edges_traversed += g.E;
+    rt.stats.direction_log.push_back(b.s1.direction);
+    GG_CUDA(cudaMemcpyAsync(&l1, sc.p + 1, 8, cudaMemcpyDeviceToHost, st));
+    GG_CUDA(cudaStreamSynchronize(st));
+  }
+  GG_CUDA(cudaMemcpyAsync(ranks_out, rank.p, V * sizeof(double), cudaMemcpyDefault, st));
+  GG_CUDA(cudaStreamSynchronize(st));
+}
+
 template <class CT>
 int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int64_t max_iters,
                          double tol, double damping, double* ranks_out, Runtime& rt,
@@ -466,6 +559,16 @@ void pagerank_run(const Graph& g, const gg_binding& b, bool fusion, const gg_exe
                           "switching applies to bfs/bc)");
   check_binding(b);
   DeviceGuard guard(g.dev);
+  if (cfg && cfg->deterministic) {  // fixed summation order, bitwise the reference's (see above)
+    if (init_ranks) {
+      DevBuf<double> ini(g.V);
+      GG_CUDA(cudaMemcpyAsync(ini.p, init_ranks, g.V * 8, cudaMemcpyDefault, rt.stream));
+      pagerank_deterministic(g, b, max_iters, tol, damping, ranks_out, rt, ini.p);
+    } else {
+      pagerank_deterministic(g, b, max_iters, tol, damping, ranks_out, rt, nullptr);
+    }
+    return;
+  }
   if (b.s1.load_balance == GG_LB_EDGE_ONLY && b.s1.blocking) {
     if (fp32_contrib)
       pagerank_blocked<float>(g, b.s1, fusion, max_iters, tol, damping, ranks_out, rt, init_ranks);

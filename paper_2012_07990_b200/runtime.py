@@ -27,9 +27,12 @@ class ExecConfig:
     """CTA hierarchy shape (runtime.py:26-50).
 
     On the device ``cta_size`` is the CTA granularity of the ETWC/TWC
-    balancers and ``warp_size`` must be 32 (hardware).  ``num_workers`` and
-    ``deterministic`` are the reference's host-simulation knobs: they are
-    validated and accepted; the grid is always sized to the GPU.
+    balancers and ``warp_size`` must be 32 (hardware).  ``num_workers`` is
+    the reference's host-simulation knob: validated and accepted, the grid is
+    always sized to the GPU.  ``deterministic`` makes ``pagerank`` sum in the
+    reference's fixed order (runtime.py:167): its ranks are then bitwise the
+    reference's for EDGE_ONLY (+ BLOCKED) and PULL schedules (slow: the
+    sequential sums run on one thread each).
     """
 
     num_workers: int = 1

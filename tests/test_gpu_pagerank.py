@@ -134,6 +134,41 @@ def test_pagerank_observed_equals_plain_run(gg, blocked):
     assert all(abs(sum(r) - 1.0) < 1e-9 for r in seen)
 
 
+def test_pagerank_deterministic_is_bitwise_the_reference(gg, golden_small, monkeypatch):
+    """ExecConfig(deterministic=True): per-destination sums in COO order, the
+    dangling mass and L1 in vertex order, every operation rounded on its own
+    (no FMA) -- the reference's own order for EDGE_ONLY (+ BLOCKED) and PULL
+    schedules, so the ranks are the reference's bit for bit
+    (runtime.py:26-50, :167; algos.py:163-208)."""
+    det = gg.ExecConfig(deterministic=True)
+    n = 0
+    for case in golden_small["cases"]:
+        if case["algo"] != "pagerank":
+            continue
+        rec = golden_small["graphs"][case["graph"]]
+        g = _graph(gg, rec)
+        sch = case["schedule"]
+        prog = None if sch is None else program_with(sched_from(sch))
+        r = gg.pagerank(g, prog, det, max_iters=case["max_iters"], tolerance=case["tolerance"])
+        if sch is None or sch["load_balance"] == "EDGE_ONLY" or sch["direction"] == "PULL":
+            assert r.values == case["ranks"], (case["graph"], sch)  # bitwise
+            n += 1
+        else:  # PUSH: the reference sums in its balancer's source order
+            assert max_rel_err(r.values, case["ranks"]) < 1e-12
+        assert r.stats.rounds == case["stats"]["rounds"]
+    assert n >= 16
+
+
+def test_pagerank_deterministic_c1_bitwise(gg):
+    z = np.load(os.path.join(GOLDEN, "c1_pagerank_rmat16.npz"))
+    g = gg.generate_rmat(16, 16, seed=1)
+    det = gg.ExecConfig(deterministic=True)
+    for sch in (None, gg.Schedule(load_balance="EDGE_ONLY", blocking=True),
+                gg.Schedule(direction="PULL", load_balance="STRICT")):
+        r = gg.pagerank(g, program_with(sch), det, max_iters=20, tolerance=0.0)
+        assert np.array_equal(r.array, z["ranks"])  # the reference's ranks, bit for bit
+
+
 def test_pagerank_errors(gg):
     g = gg.Graph.from_coo(2, [0], [1])
     with pytest.raises(gg.ScheduleError, match="hybrid"):
