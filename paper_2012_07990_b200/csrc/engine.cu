@@ -80,12 +80,21 @@ void dense_size_on_device(Frontier* f, cudaStream_t s) {
   f->size_cache = -1;
 }
 
+// the per-round frontier-size read-backs (hybrid direction choice, loop
+// end) go through a pinned per-thread word: a copy into pageable memory is
+// staged by the driver and costs several microseconds more per round
+static unsigned long long* pinned_word() {
+  static thread_local unsigned long long* w = nullptr;
+  if (!w) GG_CUDA(cudaMallocHost(&w, sizeof(unsigned long long)));
+  return w;
+}
+
 int64_t frontier_size_raw(Frontier* f, cudaStream_t s) {
   if (f->size_cache >= 0) return f->size_cache;
-  unsigned long long h = 0;
-  GG_CUDA(cudaMemcpyAsync(&h, f->count.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  unsigned long long* h = pinned_word();
+  GG_CUDA(cudaMemcpyAsync(h, f->count.p, sizeof(*h), cudaMemcpyDeviceToHost, s));
   GG_CUDA(cudaStreamSynchronize(s));
-  f->size_cache = (int64_t)h;
+  f->size_cache = (int64_t)*h;
   return f->size_cache;
 }
 
