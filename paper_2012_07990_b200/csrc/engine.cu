@@ -466,7 +466,8 @@ namespace {
 struct DevicePool {
   std::mutex mu;
   std::map<std::pair<int, size_t>, std::vector<void*>> free_blocks;
-  size_t cached = 0;
+  size_t cached = 0;                  // all devices (gg_pool_stats)
+  std::map<int, size_t> dev_cached;   // per device: compared against that device's cap
   int64_t mallocs = 0, frees = 0;
 };
 DevicePool& pool() {
@@ -488,21 +489,23 @@ size_t size_class(size_t bytes) {
 // working set: RMAT-27 PageRank end to end (COO, CSR, sort buffers, layout)
 // frees ~74 GB per call, and at a 48 GB cap every call paid 16 cudaMalloc +
 // 16 synchronising cudaFree (0.63-1.19 s per call instead of 0.61 s).
-size_t pool_limit() {
+// (per device: each device's cache is held against its own HBM size)
+size_t pool_limit(int dev) {
   const char* e = getenv("GG_POOL_MAX_GB");
   if (e) {
     const double gb = atof(e);
     return gb > 0 ? (size_t)(gb * (double)(size_t(1) << 30)) : 0;
   }
-  static const size_t dflt = [] {
-    size_t fr = 0, total = 0;
-    if (cudaMemGetInfo(&fr, &total) != cudaSuccess) {
-      cudaGetLastError();
-      return size_t(48) << 30;
-    }
-    return (size_t)(0.6 * (double)total);
-  }();
-  return dflt;
+  static std::mutex mu;
+  static std::map<int, size_t> dflt;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = dflt.find(dev);
+  if (it != dflt.end()) return it->second;
+  size_t total = size_t(80) << 30;
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) total = prop.totalGlobalMem;  // once per device
+  else cudaGetLastError();
+  return dflt[dev] = (size_t)(0.6 * (double)total);
 }
 }  // namespace
 
@@ -519,6 +522,7 @@ void pool_trim() {
   cudaSetDevice(cur);
   P.free_blocks.clear();
   P.cached = 0;
+  P.dev_cached.clear();
 }
 
 void pool_counters(int64_t* mallocs, int64_t* frees, int64_t* cached) {
@@ -541,6 +545,7 @@ void* pool_alloc(size_t bytes, size_t* granted) {
       void* q = it->second.back();
       it->second.pop_back();
       P.cached -= c;
+      P.dev_cached[dev] -= c;
       *granted = c;
       return q;
     }
@@ -578,24 +583,28 @@ void pool_free(void* q, size_t granted) {
   std::vector<std::pair<int, void*>> evict;
   {
     std::lock_guard<std::mutex> lk(P.mu);
-    if (granted > pool_limit()) {
+    const size_t lim = pool_limit(dev);
+    size_t& dc = P.dev_cached[dev];
+    if (granted > lim) {
       evict.push_back({dev, q});
     } else {
       // Make room by returning the largest cached blocks of OTHER size
       // classes: one-off temporaries (graph build sort buffers) go, while a
       // block that is freed and re-requested every call stays cached
       // (otherwise every call pays a synchronising cudaFree + cudaMalloc).
-      for (auto it = P.free_blocks.rbegin(); P.cached + granted > pool_limit() && it != P.free_blocks.rend(); ++it) {
-        if (it->first == std::make_pair(dev, granted)) continue;
-        while (!it->second.empty() && P.cached + granted > pool_limit()) {
+      for (auto it = P.free_blocks.rbegin(); dc + granted > lim && it != P.free_blocks.rend(); ++it) {
+        if (it->first.first != dev || it->first.second == granted) continue;  // this device, other sizes
+        while (!it->second.empty() && dc + granted > lim) {
           evict.push_back({it->first.first, it->second.back()});
           it->second.pop_back();
           P.cached -= it->first.second;
+          dc -= it->first.second;
         }
       }
-      if (P.cached + granted <= pool_limit()) {
+      if (dc + granted <= lim) {
         P.free_blocks[{dev, granted}].push_back(q);
         P.cached += granted;
+        dc += granted;
       } else {
         evict.push_back({dev, q});
       }
