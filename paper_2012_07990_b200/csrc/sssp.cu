@@ -325,7 +325,7 @@ __device__ __forceinline__ void far_push_one(const SsspAsyncArgs& a, int f, int3
   a.qd[f][p] = d;
 }
 
-__global__ void __launch_bounds__(256) k_sssp_async(SsspAsyncArgs a) {
+__global__ void __launch_bounds__(1024) k_sssp_async(SsspAsyncArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -838,9 +838,15 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
 
   if (fusion && s.load_balance == GG_LB_VERTEX_BASED) {
     // asynchronous bucket phases over CTA work lists (k_sssp_async)
-    int per_sm = 3;  // measured: 1 / 2 / 3 CTAs per SM = 38.1 / 34.5 / 34.0 ms (C3, delta 8192)
+    int per_sm = 2;
     if (const char* e = getenv("GG_SSSP_ASYNC_PER_SM")) per_sm = std::max(1, atoi(e));
-    const int blocks = max_coop_blocks((const void*)k_sssp_async, 256, dev, 0, per_sm);
+    // CTA size x CTAs per SM (GG_SSSP_BLOCK, GG_SSSP_ASYNC_PER_SM), measured
+    // on the C3 grid: 128 x 4..8 41-44 ms, 256 x 1/2/3 38/35/31-34 ms,
+    // 512 x 2 28.6-30 ms, 1024 x 1 29.8-31 ms -- bigger CTA work lists keep
+    // more of the wavefront local (less ring traffic, fewer idle CTAs)
+    int block = 512;
+    if (const char* e = getenv("GG_SSSP_BLOCK")) block = atoi(e) == 128 ? 128 : atoi(e) == 512 ? 512 : atoi(e) == 1024 ? 1024 : 256;
+    const int blocks = max_coop_blocks((const void*)k_sssp_async, block, dev, 0, per_sm);
     uint64_t R = 1 << 20;
     while (R < (uint64_t)(4 * V + 4096)) R <<= 1;
     // far lists: live copies (one per vertex) plus stale copies and the CTAs'
@@ -892,7 +898,7 @@ void sssp_run(const Graph& g, int64_t source, const gg_binding& b, bool fusion, 
     if (const char* e = getenv("GG_SSSP_SPILL")) a.spill = std::max(32, std::min(kLq / 4, atoi(e)));
     void* args[] = {&a};
     rt.edge_begin();
-    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_sssp_async, blocks, 256, args, 0, st));
+    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_sssp_async, blocks, block, args, 0, st));
     rt.edge_end();
     count_launch();
     long long h[3];
