@@ -625,14 +625,15 @@ void etwc_huge(Runtime* rt, EtwcEntry** q, unsigned long long** n, int64_t small
                int64_t entries) {
   rt->g->ensure_out();
   // no hub and a frontier that fills the grid: no grid pass (no extra barriers)
-  if (rt->g->max_out_degree < kEtwcHuge && (small_frontier == 0 || rt->g->max_out_degree < rt->cfg.cta_size)) {
+  if (rt->g->max_out_degree < kEtwcHuge && (small_frontier == 0 || rt->g->max_out_degree < kWarp)) {
     *q = nullptr;
     *n = nullptr;
     return;
   }
   // one entry per active-list entry at most (a multiset frontier -- dedup
-  // off -- repeats a hub once per occurrence), per kEtwcHuge arcs otherwise
-  const int64_t cap = std::max({rt->g->E / kEtwcHuge, small_frontier, entries}) + 1;
+  // off -- repeats a hub once per occurrence), per kEtwcHuge arcs otherwise;
+  // a small frontier queues each vertex's CTA- and warp-stage ranges (two)
+  const int64_t cap = std::max({rt->g->E / kEtwcHuge, 2 * small_frontier, 2 * entries}) + 1;
   if (rt->etwc_q.n < (size_t)cap) rt->etwc_q.alloc(cap);
   if (!rt->etwc_n.p) rt->etwc_n.alloc(1);
   GG_CUDA(cudaMemsetAsync(rt->etwc_n.p, 0, sizeof(unsigned long long), rt->stream));

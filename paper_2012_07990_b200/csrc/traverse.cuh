@@ -667,6 +667,14 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
       a.huge[atomicAdd(a.huge_n, 1ULL)] = c2;
       e2 = 0;
     }
+    // small frontier (huge_min lowered to the CTA size): the warp-stage
+    // ranges go to the grid pass as well -- a few hundred frontier vertices
+    // fill one CTA, whose 8 warps otherwise walk every vertex's warp stage
+    // (a 246-vertex RMAT-24 BFS level: 328 us in that one CTA)
+    if (a.huge && a.huge_min <= cta && e1 > 0) {
+      a.huge[atomicAdd(a.huge_n, 1ULL)] = c1;
+      e1 = 0;
+    }
     bool has[3] = {e0 > 0, e1 > 0, e2 > 0};
     const EtwcEntry* ent[3] = {&c0, &c1, &c2};
 #pragma unroll
