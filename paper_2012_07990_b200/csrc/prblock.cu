@@ -939,9 +939,10 @@ int64_t pagerank_blocked(const Graph& g, const gg_schedule& s, bool fusion, int6
   } else {
     DevBuf<int64_t> iters(1), segs(L->K + 1);
     GG_CUDA(cudaMemcpyAsync(segs.p, L->seg_edge.data(), (L->K + 1) * 8, cudaMemcpyHostToDevice, st));
-    // 2 CTAs per SM: a grid barrier per segment and per vertex pass dominates
-    // small graphs (C1 RMAT-16: 73 / 73 / 80 / 77 GTEPS at 8 / 4 / 2 / 1 per SM)
-    int blocks = max_coop_blocks((const void*)k_prb_fused<CT>, 256, dev, 0, 2);
+    // small graphs: 2 CTAs per SM -- a grid barrier per segment and per vertex
+    // pass dominates (C1 RMAT-16: 73 / 73 / 80 / 77 GTEPS at 8 / 4 / 2 / 1 per
+    // SM); large ones keep every resident CTA for the edge stream
+    int blocks = max_coop_blocks((const void*)k_prb_fused<CT>, 256, dev, 0, g.E < (int64_t(1) << 26) ? 2 : 0);
     const int32_t* sp = L->src.p;
     const int32_t* dp = L->dst.p;
     const int64_t* se = segs.p;
