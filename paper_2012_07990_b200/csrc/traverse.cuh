@@ -505,7 +505,19 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
                                                    int64_t first, int64_t stride, bool warp_uniform = true) {
   int64_t e = lo + first;
   if constexpr (PushReduce<Op>::value) {
+    // 4 arcs in flight: their (dependent) id -> filter -> state chains are
+    // independent of each other (BC backward was latency-bound, one chain
+    // per thread: long_scoreboard 75%)
     double acc = 0.0;
+    for (; e + 3 * stride < hi; e += 4 * stride) {
+      int32_t v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldg(a.g.nbr + e + k * stride);
+      double x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k] = (a.use_filter && !a.op.filter(v[k])) ? 0.0 : a.op.push_val(u, v[k]);
+      acc += (x[0] + x[1]) + (x[2] + x[3]);
+    }
     for (; e < hi; e += stride) {
       const int32_t v = __ldg(a.g.nbr + e);
       if (a.use_filter && !a.op.filter(v)) continue;
