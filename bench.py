@@ -76,6 +76,7 @@ def parse():
                         "already admits each vertex once, so the frontier is identical)")
     p.add_argument("--pull-lb", default="VERTEX_BASED", help="c2 pull-side load balance")
     p.add_argument("--push-creation", default="FUSED", help="c2 push-side frontier creation")
+    p.add_argument("--bc-theta", type=float, default=0.01, help="c4 BC hybrid threshold")
     p.add_argument("--fusion", action="store_true", help="c1/c2/c5: fused loop (s0 kernel fusion)")
     p.add_argument("--side", type=int, default=None, help="c3 grid side")
     p.add_argument("--delta", type=int, default=None, help="c3 bucket width (default: sweep)")

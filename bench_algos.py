@@ -454,7 +454,7 @@ def cc_bc_c4(gg, args, peak):
         # "EB" = EDGE_ONLY + BLOCKED (EdgeBlocking, blocking.py:78-186), "EDGE" = EDGE_ONLY,
         # "HYBRID" = BC only: PUSH+ETWC below 1% of V, PULL+BITMAP above (CC takes no hybrid)
         if lb == "HYBRID":
-            hy = gg.HybridSchedule(threshold=0.01,
+            hy = gg.HybridSchedule(threshold=args.bc_theta,
                                    s1=gg.Schedule(direction="PUSH", load_balance="ETWC"),
                                    s2=gg.Schedule(direction="PULL", pull_frontier_repr="BITMAP",
                                                   frontier_creation="UNFUSED_BITMAP"))
