@@ -544,6 +544,64 @@ __device__ __forceinline__ void pr_edges_seg(const int32_t* __restrict__ src, co
   }
 }
 
+// All cold segments in ONE launch (Alg. 2 without the barrier between
+// segments): the segments' warp steps are concatenated in segment order and
+// dealt to warps cyclically, so the grid sweeps segment 1, then 2, ...
+// together (the L2 window moves as in the per-segment launches) while the
+// warps that finish a segment early start the next one instead of idling at
+// the launch boundary.  A step never straddles two segments, so the
+// destination order inside a step -- the segmented scan's invariant -- holds.
+constexpr int kMaxColdSegs = 48;
+struct ColdSegs {
+  int64_t a[kMaxColdSegs];  // 8-aligned first edge (steps start here)
+  int64_t e0[kMaxColdSegs], e1[kMaxColdSegs];
+  int64_t s0[kMaxColdSegs + 1];  // first global step of each segment; s0[n] = total
+  int n;
+};
+__device__ __forceinline__ void cold_step(const ColdSegs& cs, int64_t s, int64_t& base, int64_t& e0, int64_t& e1) {
+  int k = 0;
+  while (k + 1 < cs.n && s >= cs.s0[k + 1]) ++k;
+  base = cs.a[k] + (s - cs.s0[k]) * (32 * kE);
+  e0 = cs.e0[k];
+  e1 = cs.e1[k];
+}
+template <class CT>
+static __global__ void __launch_bounds__(256) k_pr_edges_cold(const int32_t* __restrict__ src,
+                                                            const int32_t* __restrict__ dst, const __grid_constant__ ColdSegs cs,
+                                                            const CT* contrib, double* acc) {
+  const int lane = lane_id();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = cs.s0[cs.n];
+  int64_t s = warp;
+  if (s >= total) return;
+  int64_t base, e0, e1;
+  cold_step(cs, s, base, e0, e1);
+  int32_t su[kE], dv[kE];
+  pr_load_edges(src, dst, base + lane * kE, e0, e1, su, dv);
+  for (; s < total; s += nwarps) {
+    int32_t nsu[kE], ndv[kE];
+    const int64_t sn = s + nwarps;
+    if (sn < total) {
+      int64_t nb, n0, n1;
+      cold_step(cs, sn, nb, n0, n1);
+      pr_load_edges(src, dst, nb + lane * kE, n0, n1, nsu, ndv);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kE; ++q) {
+        nsu[q] = 0;
+        ndv[q] = -1;
+      }
+    }
+    pr_reduce_step<CT, false>(su, dv, contrib, acc, 0, nullptr, 0);
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      su[q] = nsu[q];
+      dv[q] = ndv[q];
+    }
+  }
+}
+
 template <class CT, bool kPrefetch, int kMinBlocks = 1>
 static __global__ void __launch_bounds__(256, kMinBlocks) k_pr_edges(const int32_t* src, const int32_t* dst,
                                                                      int64_t e0, int64_t e1, const CT* contrib,
@@ -721,6 +779,7 @@ struct HotCfg {
   int gather = 0;
   int32_t cold_from = INT32_MAX;  // one-segment layout: first source past the L2 window
   int cold_minb = 0;              // cold-segment kernel register cap (GG_PR_COLD_MINB)
+  bool cold_one = false;          // all cold segments in one launch (GG_PR_COLD_ONE)
   unsigned grid = 0, hot_grid = 0;
 };
 
@@ -773,6 +832,7 @@ static HotCfg hot_cfg(int dev, const PrBlockLayout* L) {
   // CTAs per SM (default: the compiler's 64 registers, 4 per SM); the grid
   // is GG_PR_COLD_GRID CTAs per SM (default 8)
   if (const char* e = getenv("GG_PR_COLD_MINB")) h.cold_minb = atoi(e);
+  if (const char* e = getenv("GG_PR_COLD_ONE")) h.cold_one = atoi(e) != 0;
   int per = 8;
   if (const char* e = getenv("GG_PR_COLD_GRID")) per = std::max(1, atoi(e));
   h.grid = (unsigned)sm_count(dev) * per;
@@ -829,9 +889,35 @@ struct PrRank {
   void edges(int64_t it, cudaStream_t st, int which = 0) {
     NvtxRange nvtx("gg.pr_block.edge_phase");
     const CT* c = cur(it);
+    bool cold_done = false;
+    if (hc.cold_one && which != 1 && hc.prefetch) {
+      ColdSegs cs;
+      cs.n = 0;
+      int64_t steps = 0;
+      for (int64_t k = 1; k < L->K && cs.n < kMaxColdSegs; ++k) {
+        const int64_t e0 = L->seg_edge[k], e1 = L->seg_edge[k + 1];
+        if (e1 <= e0) continue;
+        const int64_t a = e0 & ~int64_t(kE - 1);
+        cs.a[cs.n] = a;
+        cs.e0[cs.n] = e0;
+        cs.e1[cs.n] = e1;
+        cs.s0[cs.n] = steps;
+        steps += (e1 - a + 32 * kE - 1) / (32 * kE);
+        ++cs.n;
+      }
+      cs.s0[cs.n] = steps;
+      if (L->K - 1 <= kMaxColdSegs) {
+        cold_done = true;
+        if (cs.n > 0) {
+          k_pr_edges_cold<CT><<<hc.grid, 256, 0, st>>>(L->src.p, L->dst.p, cs, c, acc);
+          ++launches;
+        }
+      }
+    }
     for (int64_t k = 1; k <= L->K; ++k) {
       const int64_t sg = k == L->K ? 0 : k;
       if ((which == 1 && sg != 0) || (which == 2 && sg == 0)) continue;
+      if (cold_done && sg != 0) continue;
       const int64_t e0 = L->seg_edge[sg], e1 = L->seg_edge[sg + 1];
       if (e1 <= e0) continue;
       cudaEvent_t ta = nullptr, tb = nullptr;

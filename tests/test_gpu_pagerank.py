@@ -75,6 +75,22 @@ def test_pagerank_edge_blocking_matches_oracle(gg, n, fusion):
     assert max_rel_err(r.values, want) < PR_TOL
 
 
+@pytest.mark.parametrize("cold_one", ["0", "1"])
+@pytest.mark.parametrize("n", [1, 64, 200, 1000])
+def test_pagerank_edge_blocking_cold_segments_one_launch(gg, n, cold_one, monkeypatch):
+    """GG_PR_COLD_ONE=1 runs every cold segment in one launch (steps dealt in
+    segment order); more segments than the launch parameter holds (n=1)
+    falls back to one launch per segment."""
+    monkeypatch.setenv("GG_PR_COLD_ONE", cold_one)
+    V, s, d = gen.rmat(12, 8, seed=13)
+    g = gg.Graph.from_coo(V, s, d)
+    want, _ = oracle.pagerank(V, s, d, 20, 0.0)
+    for fp32 in (False, True):
+        sch = gg.Schedule(load_balance="EDGE_ONLY", blocking=True, blocking_size=n)
+        r = gg.pagerank(g, program_with(sch), max_iters=20, tolerance=0.0, contrib_fp32=fp32)
+        assert max_rel_err(r.array, want) < PR_TOL
+
+
 def test_c1_rmat16_device_generator_and_ranks(gg):
     """C1 (BASELINE configs[0]): the device RMAT generator is bit-identical to
     the fixture's edge list and 20 iterations match the reference's ranks."""

@@ -10,6 +10,7 @@
 #   smoke              __graft_entry__.smoke()
 #   bench[=ARGS]       python bench.py ARGS (default: the driver's default run)
 #   launches[=ARGS]    ncu launch list (gpu__time_duration) of bench.py ARGS
+#   launchesw[=ARGS]   same, --cache-control none (warm caches between launches)
 #   ncu=REGEX@ARGS     ncu --set full of the first launch matching REGEX
 #   py=SCRIPT@ARGS     python SCRIPT ARGS
 # Arguments use ',' for spaces (bench=--config,c2,--check).
@@ -35,10 +36,16 @@ for step in "$@"; do
     launches)
       timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
         --clock-control none --csv --log-file $out.csv python bench.py $arg > $out.txt 2>&1 ;;
+    launchesw)
+      timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --cache-control none --csv --log-file $out.csv python bench.py $arg > $out.txt 2>&1 ;;
     ncu)
       re=${arg%%@*}; a=${arg#*@}
       timeout 1800 ncu --set full --clock-control none --import-source on -k "regex:$re" -c 1 \
-        -o $out python bench.py $a > $out.txt 2>&1 ;;
+        -o $out python bench.py $a > $out.txt 2>&1
+      # the binary report may not survive the trip back: summarise it here
+      ncu -i $out.ncu-rep --page raw --csv > $out.raw.csv 2>&1
+      python tools/ncu_summary.py $out.summary.txt $out.ncu-rep > /dev/null 2>&1 ;;
     py)
       s=${arg%%@*}; a=""; [[ "$arg" == *@* ]] && a=${arg#*@}
       timeout 1800 python $s $a > $out.txt 2>&1; echo "rc=$?" >> $out.txt ;;
