@@ -83,6 +83,7 @@ def parse():
     p.add_argument("--lb", default="VERTEX_BASED",
                    help="c3 load balance (VERTEX_BASED runs the asynchronous bucket phases; swept best)")
     p.add_argument("--no-fusion", action="store_true", help="c3: unfused loop")
+    p.add_argument("--no-bc", action="store_true", help="c4: CC only (profiling)")
     p.add_argument("--lbs", default="ETWC,TWC,VERTEX_BASED,EB,EDGE,HYBRID",
                    help="c4 load balances (EB = EDGE_ONLY+BLOCKED, EDGE = EDGE_ONLY)")
     p.add_argument("--no-sub", action="store_true", help="c5: skip the C1-C4 sub-runs")

@@ -484,7 +484,7 @@ def cc_bc_c4(gg, args, peak):
                       "gteps": st.edges_traversed / (m * 1e-3) / 1e9,
                       "frac": ((4.0 * A + 16.0 * V) * st.rounds / (m * 1e-3) / 1e9) / peak}
         cc_bad[lb] = int(np.count_nonzero(labels.cpu().numpy() != want_cc))
-        if lb in ("EB", "EDGE"):  # frontier traversals: EDGE_ONLY would scan every arc per level
+        if lb in ("EB", "EDGE") or getattr(args, "no_bc", False):  # frontier traversals: EDGE_ONLY would scan every arc per level
             continue
         gg.bc(g, bc_sources[:1], prog, out=scores)
         r, ms_bc = _bc_timed(gg, g, bc_sources, prog, scores)

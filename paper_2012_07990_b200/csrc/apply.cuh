@@ -5,6 +5,14 @@
 
 namespace gg {
 
+template <class Op>
+inline void launch_push_huge(const PushArgs<Op>& a, int dev, cudaStream_t st) {
+  if constexpr (MinBlocks<Op>::value > 1)
+    k_push_huge_mb<Op, MinBlocks<Op>::value><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+  else
+    k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+}
+
 int max_coop_blocks(const void* fn, int block, int dev, size_t smem = 0, int cap_per_sm = 0);
 void strict_prefix(Runtime* rt, const InView& in, int64_t n);
 void strict_spans(Runtime* rt, int64_t nspans);
@@ -64,9 +72,12 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
       const bool small = work < kEtwcSmallPerSm * sm_count(dev);
       etwc_huge(rt, &a.huge, &a.huge_n, small ? work : 0, work);
       if (small && a.huge) a.huge_min = cta;
-      k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
+      if constexpr (MinBlocks<Op>::value > 1)
+        k_push_etwc_mb<Op, MinBlocks<Op>::value><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
+      else
+        k_push_etwc<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, cta);
       if (a.huge) {
-        k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+        launch_push_huge<Op>(a, dev, st);
         count_launch();
       }
       break;
@@ -83,12 +94,19 @@ void run_push(Runtime* rt, const gg_schedule& s, const Op& op, bool use_filter, 
       etwc_huge(rt, &a.huge, &a.huge_n, 0, work);  // hubs skip the bins (b_twc_bin)
       k_twc_bin<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q, cta);
       a.scanned = rt->scanned.p;
-      k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
-      k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
-      k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      if constexpr (MinBlocks<Op>::value > 1) {
+        constexpr int mb = MinBlocks<Op>::value;
+        k_twc_thread_mb<Op, mb><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
+        k_twc_warp_mb<Op, mb><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
+        k_twc_cta_mb<Op, mb><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      } else {
+        k_twc_thread<Op><<<grid_for(work, 256, dev), 256, 0, st>>>(a, q.q[0], q.cnt);
+        k_twc_warp<Op><<<grid_for(work * 32, 256, dev), 256, 0, st>>>(a, q.q[1], q.cnt + 1);
+        k_twc_cta<Op><<<grid_for(work * 256, 256, dev), 256, 0, st>>>(a, q.q[2], q.cnt + 2);
+      }
       count_launch(3);
       if (a.huge) {
-        k_push_huge<Op><<<(unsigned)sm_count(dev) * 8, 256, 0, st>>>(a);
+        launch_push_huge<Op>(a, dev, st);
         count_launch();
       }
       break;

@@ -101,6 +101,10 @@ void cc_run(const Graph& g, const gg_binding& b, bool fusion, Runtime& rt, int32
     cc_fused(rt, b.s1, label.p, flags.p);
   } else {
     OpHook op{label.p, flags.p};
+    {
+      const char* rs = getenv("GG_CC_ROOT_SKIP");
+      op.root_skip = !(rs && atoi(rs) == 0);
+    }
     // giant-component filter (OpHook::giant), rebuilt after every round's
     // pointer jumping; none before the first round (labels are the ids)
     const int64_t W = (V + 31) / 32;

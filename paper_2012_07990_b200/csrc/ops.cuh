@@ -124,6 +124,15 @@ struct OpHook {
   // one tree to itself, so its two random label reads are skipped (an
   // L2-resident bit test instead: most arcs after the first round)
   const uint32_t* giant = nullptr;
+  // root shortcut: when the larger label is the random endpoint v's own id
+  // (label[v] == v, just read), label[hi] is known to be hi > lo, so the
+  // re-read before the atomic is skipped (one L2 request per arc less in
+  // the first round, where most vertices are still roots).  Not applied to
+  // u: lanes of a warp share u, so its re-read is one coalesced request,
+  // while one atomic per lane on a hub's label would serialise.
+  bool root_skip = false;
+  static constexpr bool kPush4 = true;
+  static constexpr int kMinBlocks = 8;  // 32 registers: full residency (latency-bound chains)
   using Acc = int;
   static constexpr bool kEarlyExit = false;
   __device__ __forceinline__ bool filter(int32_t) const { return true; }
@@ -134,13 +143,45 @@ struct OpHook {
     int32_t lo = la < lb ? la : lb, hi = la < lb ? lb : la;
     // skip hooks that cannot lower label[hi] (hub roots receive one hook per
     // incident arc; only the smaller ones need the atomic)
-    if (lo >= *((volatile int32_t*)label + hi)) return;
+    if (!(root_skip && hi == v && lb == v) && lo >= *((volatile int32_t*)label + hi)) return;
     // read before write: one hot flag line, written once per round instead of
     // once per successful hook (which serialises at its L2 slice)
     if (atomicMin(label + hi, lo) > lo && !*((volatile int*)changed)) *changed = 1;
   }
   __device__ __forceinline__ void push(int32_t u, int32_t v, uint32_t, const OutBuilder&) const {
     hook(u, v);
+  }
+  // hook() for 4 arcs of one source: the same tests and atomic per arc, with
+  // each step's 4 loads issued together (label[u] read once per batch)
+  __device__ __forceinline__ void push4(int32_t u, const int32_t (&v)[4], unsigned live) const {
+    if (giant && ((__ldg(giant + (u >> 5)) >> (u & 31)) & 1u)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((live >> k) & 1u) && ((__ldg(giant + (v[k] >> 5)) >> (v[k] & 31)) & 1u)) live &= ~(1u << k);
+    }
+    if (!live) return;
+    const int32_t la = *((volatile int32_t*)label + u);
+    int32_t lb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lb[k] = ((live >> k) & 1u) ? *((volatile int32_t*)label + v[k]) : la;
+    int32_t lo[4], hi[4], cur[4];
+    unsigned need = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      lo[k] = la < lb[k] ? la : lb[k];
+      hi[k] = la < lb[k] ? lb[k] : la;
+      if (lb[k] != la) need |= 1u << k;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool known_root = root_skip && hi[k] == v[k] && lb[k] == v[k];
+      cur[k] = ((need >> k) & 1u) && !known_root ? *((volatile int32_t*)label + hi[k]) : INT32_MAX;
+    }
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((need >> k) & 1u) && lo[k] < cur[k]) any |= atomicMin(label + hi[k], lo[k]) > lo[k];
+    if (any && !*((volatile int*)changed)) *changed = 1;
   }
   __device__ __forceinline__ Acc init() const { return 0; }
   __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t) const {

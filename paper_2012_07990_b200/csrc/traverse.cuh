@@ -219,6 +219,20 @@ __device__ __forceinline__ void push_edge(const PushArgs<Op>& a, int32_t u, int6
   a.op.push(u, v, w, a.out);
 }
 
+// cooperative range walk (defined with the ETWC stages below); ops may pin
+// the traversal kernels' residency (kMinBlocks CTAs of 256 per SM: a
+// register cap, the *_mb kernel twins) when their chains are latency-bound.
+// Ops that do not declare it launch the plain kernels: an explicit minimum
+// of 1 would lift the compiler's own register budget (BC kernels went from
+// 32-48 to 58-70 registers and ~12% slower, measured)
+template <class Op>
+__device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_t u, int64_t lo, int64_t hi,
+                                                   int64_t first, int64_t stride, bool warp_uniform = true);
+template <class, class = void>
+struct MinBlocks : std::integral_constant<int, 1> {};
+template <class T>
+struct MinBlocks<T, std::void_t<decltype(T::kMinBlocks)>> : std::integral_constant<int, T::kMinBlocks> {};
+
 // VERTEX_BASED (engine.py:179-183): one thread per active vertex.
 template <class Op>
 __device__ __forceinline__ void b_push_vb(PushArgs<Op> a) {
@@ -428,12 +442,17 @@ __device__ __forceinline__ void b_twc_thread(PushArgs<Op> a, const int32_t* qu,
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t u = qu[i];
     int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
-    for (int64_t e = lo; e < hi; ++e) push_edge(a, u, e);
+    push_range_strided(a, u, lo, hi, 0, 1, false);
   }
 }
 template <class Op>
 __global__ void __launch_bounds__(256) k_twc_thread(PushArgs<Op> a, const int32_t* qu,
                                                     const unsigned long long* cnt) {
+  b_twc_thread<Op>(a, qu, cnt);
+}
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_twc_thread_mb(PushArgs<Op> a, const int32_t* qu,
+                                                             const unsigned long long* cnt) {
   b_twc_thread<Op>(a, qu, cnt);
 }
 
@@ -446,12 +465,17 @@ __device__ __forceinline__ void b_twc_warp(PushArgs<Op> a, const int32_t* qu,
   for (int64_t i = warp; i < n; i += nwarps) {
     int32_t u = qu[i];
     int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
-    for (int64_t e = lo + lane_id(); e < hi; e += kWarp) push_edge(a, u, e);
+    push_range_strided(a, u, lo, hi, lane_id(), kWarp);
   }
 }
 template <class Op>
 __global__ void __launch_bounds__(256) k_twc_warp(PushArgs<Op> a, const int32_t* qu,
                                                   const unsigned long long* cnt) {
+  b_twc_warp<Op>(a, qu, cnt);
+}
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_twc_warp_mb(PushArgs<Op> a, const int32_t* qu,
+                                                           const unsigned long long* cnt) {
   b_twc_warp<Op>(a, qu, cnt);
 }
 
@@ -466,12 +490,17 @@ __device__ __forceinline__ void b_twc_cta(PushArgs<Op> a, const int32_t* qu,
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     int32_t u = qu[i];
     int64_t lo = __ldg(a.g.off + u), hi = __ldg(a.g.off + u + 1);
-    for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) push_edge(a, u, e);
+    push_range_strided(a, u, lo, hi, threadIdx.x, blockDim.x);
   }
 }
 template <class Op>
 __global__ void __launch_bounds__(256) k_twc_cta(PushArgs<Op> a, const int32_t* qu,
                                                  const unsigned long long* cnt) {
+  b_twc_cta<Op>(a, qu, cnt);
+}
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_twc_cta_mb(PushArgs<Op> a, const int32_t* qu,
+                                                          const unsigned long long* cnt) {
   b_twc_cta<Op>(a, qu, cnt);
 }
 
@@ -497,12 +526,21 @@ template <class, class = void>
 struct PushReduce : std::false_type {};
 template <class T>
 struct PushReduce<T, std::void_t<decltype(T::kPushReduce)>> : std::integral_constant<bool, T::kPushReduce> {};
+// Ops whose per-arc work is a chain of dependent loads (CC hook: label[v],
+// then label[max], then the atomic) declare kPush4 and provide push4(u, v[4],
+// live mask): a range walk hands them 4 arcs at once so the 4 chains' loads
+// are in flight together (the hook round was latency-bound: long_scoreboard
+// 68%, one chain per thread).  Unweighted ops only.
+template <class, class = void>
+struct PushBatch : std::false_type {};
+template <class T>
+struct PushBatch<T, std::void_t<decltype(T::kPush4)>> : std::integral_constant<bool, T::kPush4> {};
 
 // Cooperative range walk with 4 independent arcs in flight per thread.
 // `warp_uniform`: every lane of the warp walks the same source u.
 template <class Op>
 __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_t u, int64_t lo, int64_t hi,
-                                                   int64_t first, int64_t stride, bool warp_uniform = true) {
+                                                   int64_t first, int64_t stride, bool warp_uniform) {
   int64_t e = lo + first;
   if constexpr (PushReduce<Op>::value) {
     // 4 arcs in flight: their (dependent) id -> filter -> state chains are
@@ -528,6 +566,20 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
       if (lane_id() == 0 && acc != 0.0) a.op.push_commit(u, acc);
     } else if (acc != 0.0) {
       a.op.push_commit(u, acc);
+    }
+    return;
+  }
+  if constexpr (PushBatch<Op>::value) {
+    for (; e < hi; e += 4 * stride) {
+      int32_t v[4];
+      unsigned live = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool in = e + k * stride < hi;
+        v[k] = in ? __ldg(a.g.nbr + e + k * stride) : 0;
+        if (in && (!a.use_filter || a.op.filter(v[k]))) live |= 1u << k;
+      }
+      a.op.push4(u, v, live);
     }
     return;
   }
@@ -649,6 +701,10 @@ template <class Op>
 __global__ void __launch_bounds__(256) k_push_huge(PushArgs<Op> a) {
   b_push_huge<Op>(a);
 }
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_push_huge_mb(PushArgs<Op> a) {
+  b_push_huge<Op>(a);
+}
 
 template <class Op>
 __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
@@ -719,6 +775,10 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
 }
 template <class Op>
 __global__ void __launch_bounds__(256) k_push_etwc(PushArgs<Op> a, int cta) {
+  b_push_etwc<Op>(a, cta);
+}
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_push_etwc_mb(PushArgs<Op> a, int cta) {
   b_push_etwc<Op>(a, cta);
 }
 
