@@ -429,7 +429,9 @@ def cc_bc_c4(gg, args, peak):
     V, A = g.num_vertices, g.num_edges
     deg = np.diff(np.asarray(g.out_offsets, dtype=np.int64))
     s_h, d_h = g.coo_src.copy(), g.coo_dst.copy()
-    lbs = args.lbs.split(",")
+    lbs = args.lbs.replace("+", ",").split(",")  # "+" also separates (tools/gpu.sh turns "," into spaces)
+    if not any(lb != "HYBRID" for lb in lbs):
+        raise SystemExit("--lbs needs a CC load balance besides HYBRID (ETWC, TWC, VERTEX_BASED, EB, EDGE)")
     labels = torch.empty(V, dtype=torch.int32, device="cuda")
     scores = torch.empty(V, dtype=torch.float64, device="cuda")
     bc_sources = _pick_sources(deg, args.sources or 4, 6)
@@ -500,10 +502,10 @@ def cc_bc_c4(gg, args, peak):
               "ok": (all(v == 0 for v in cc_bad.values())
                      and all(v <= 1e-5 for v in bc_err.values()))}
 
-    head = lbs[0]
+    head = next(lb for lb in lbs if lb != "HYBRID")  # the headline is a CC run
     prog = gg.ScheduleProgram({"s0:s1": gg.Schedule(direction="PUSH", load_balance=head)
-                               if head not in ("EB", "EDGE", "HYBRID") else
-                               gg.Schedule(load_balance="EDGE_ONLY")})
+                               if head not in ("EB", "EDGE") else
+                               gg.Schedule(load_balance="EDGE_ONLY", blocking=head == "EB")})
     # e2e: pinned host COO -> Graph.from_coo (symmetric) -> CC -> labels on host
     g.close()
     (a, sh), (b_, dh) = _pinned(s_h, d_h)

@@ -153,7 +153,8 @@ struct OpHook {
   }
   // hook() for 4 arcs of one source: the same tests and atomic per arc, with
   // each step's 4 loads issued together (label[u] read once per batch)
-  __device__ __forceinline__ void push4(int32_t u, const int32_t (&v)[4], unsigned live) const {
+  __device__ __forceinline__ void push4(int32_t u, const int32_t (&v)[4], unsigned live, int,
+                                        const OutBuilder&) const {  // filter(): always true
     if (giant && ((__ldg(giant + (u >> 5)) >> (u & 31)) & 1u)) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -334,6 +335,39 @@ struct OpBcFwdAoS {
     const int32_t nl = level + 1;
     if (*((volatile int32_t*)&st[v].depth) == -1 && atomicCAS(&st[v].depth, -1, nl) == -1) out.emit(v);
     if (*((volatile int32_t*)&st[v].depth) == nl) atomicAdd(&st[v].sigma, st[u].sigma);
+  }
+  // filter + push for 4 arcs of one source with each step's memory
+  // operations issued together (bit tests, depth reads, CAS, sigma adds).
+  // Only this round writes depths, all to level + 1, so after a CAS the
+  // depth is level + 1 whoever won: the re-read of push() is not needed.
+  static constexpr bool kPush4 = true;
+  static constexpr int kMinBlocks = 8;  // 32 registers (6 CTAs at 40: measured equal or slower)
+  __device__ __forceinline__ void push4(int32_t u, const int32_t (&v)[4], unsigned live, int use_filter,
+                                        const OutBuilder& out) const {
+    const int32_t nl = level + 1;
+    if (use_filter) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((live >> k) & 1u) && bm_has(vis, v[k])) live &= ~(1u << k);
+    }
+    if (!live) return;
+    int32_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = ((live >> k) & 1u) ? *((volatile int32_t*)&st[v[k]].depth) : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((live >> k) & 1u) && use_filter && d[k] != -1 && d[k] != nl) live &= ~(1u << k);
+    int32_t old[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) old[k] = ((live >> k) & 1u) && d[k] == -1 ? atomicCAS(&st[v[k]].depth, -1, nl) : d[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((live >> k) & 1u) && d[k] == -1 && old[k] == -1) out.emit(v[k]);
+    const double su = st[u].sigma;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((live >> k) & 1u) && (d[k] == -1 || d[k] == nl) && (old[k] == -1 || old[k] == nl))
+        atomicAdd(&st[v[k]].sigma, su);
   }
   __device__ __forceinline__ Acc init() const { return {0.0, 0}; }
   __device__ __forceinline__ bool visit(Acc& a, int32_t, int32_t u, uint32_t) const {

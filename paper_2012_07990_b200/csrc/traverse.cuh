@@ -530,7 +530,8 @@ struct PushReduce<T, std::void_t<decltype(T::kPushReduce)>> : std::integral_cons
 // then label[max], then the atomic) declare kPush4 and provide push4(u, v[4],
 // live mask): a range walk hands them 4 arcs at once so the 4 chains' loads
 // are in flight together (the hook round was latency-bound: long_scoreboard
-// 68%, one chain per thread).  Unweighted ops only.
+// 68%, one chain per thread); push4 applies the op's filter (when the apply
+// has one) to the batch itself.  Unweighted ops only.
 template <class, class = void>
 struct PushBatch : std::false_type {};
 template <class T>
@@ -577,9 +578,9 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
       for (int k = 0; k < 4; ++k) {
         const bool in = e + k * stride < hi;
         v[k] = in ? __ldg(a.g.nbr + e + k * stride) : 0;
-        if (in && (!a.use_filter || a.op.filter(v[k]))) live |= 1u << k;
+        if (in) live |= 1u << k;
       }
-      a.op.push4(u, v, live);
+      a.op.push4(u, v, live, a.use_filter, a.out);  // applies the filter itself, batched
     }
     return;
   }
