@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgg.so")
+LIB_PATH = os.environ.get("GG_LIB_PATH") or os.path.join(_HERE, "libgg.so")  # override: A/B builds
 
 # status codes (gg.h)
 GG_OK = 0

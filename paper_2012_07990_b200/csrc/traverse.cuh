@@ -812,39 +812,57 @@ __device__ __forceinline__ bool pull_visit(const PullArgs<Op>& a, typename Op::A
 // (A two-phase variant -- per-thread probe of the first two in-arcs, then
 // warp-cooperative scans of the unsettled destinations -- measured 3x slower
 // on the first RMAT-24 bottom-up level: 1.52 vs 0.52 ms.)
+#ifndef GG_PULL_K
+#define GG_PULL_K 2
+#endif
+constexpr int kPullK = GG_PULL_K;  // bottom-up destinations per thread in lock step
 template <class Op>
 __device__ __forceinline__ void b_pull_vb(PullArgs<Op> a) {
   if constexpr (Op::kEarlyExit) {
-    // early-exit ops: two destinations per thread, probed in lock step, so
-    // each thread keeps two independent in-list walks (neighbour id, then
+    // early-exit ops: kPullK destinations per thread, probed in lock step, so
+    // each thread keeps kPullK independent in-list walks (neighbour id, then
     // frontier bit) in flight -- the kernel is latency-bound
     int64_t sc = 0;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < a.g.V; v0 += 2 * nth) {
-      const int64_t v1 = v0 + nth;
-      const bool a0 = !a.use_filter || a.op.filter((int32_t)v0);
-      const bool a1 = v1 < a.g.V && (!a.use_filter || a.op.filter((int32_t)v1));
-      int64_t e0 = 0, h0 = 0, e1 = 0, h1 = 0;
-      if (a0) { e0 = __ldg(a.g.off + v0); h0 = __ldg(a.g.off + v0 + 1); sc += h0 - e0; }
-      if (a1) { e1 = __ldg(a.g.off + v1); h1 = __ldg(a.g.off + v1 + 1); sc += h1 - e1; }
-      typename Op::Acc acc0 = a.op.init(), acc1 = a.op.init();
-      bool d0 = e0 >= h0, d1 = e1 >= h1;
-      while (!d0 || !d1) {
-        const int32_t u0 = d0 ? 0 : __ldg(a.g.nbr + e0);
-        const int32_t u1 = d1 ? 0 : __ldg(a.g.nbr + e1);
-        const bool m0 = !d0 && a.in.member(u0);
-        const bool m1 = !d1 && a.in.member(u1);
-        if (!d0) {
-          const uint32_t w = a.g.w ? __ldg(a.g.w + e0) : 0u;
-          if ((m0 && a.op.visit(acc0, (int32_t)v0, u0, w)) || ++e0 >= h0) d0 = true;
+    for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < a.g.V; v0 += kPullK * nth) {
+      bool act[kPullK], done[kPullK];
+      int64_t e[kPullK], h[kPullK];
+      typename Op::Acc acc[kPullK];
+#pragma unroll
+      for (int k = 0; k < kPullK; ++k) {
+        const int64_t v = v0 + k * nth;
+        act[k] = v < a.g.V && (!a.use_filter || a.op.filter((int32_t)v));
+        e[k] = 0;
+        h[k] = 0;
+        if (act[k]) {
+          e[k] = __ldg(a.g.off + v);
+          h[k] = __ldg(a.g.off + v + 1);
+          sc += h[k] - e[k];
         }
-        if (!d1) {
-          const uint32_t w = a.g.w ? __ldg(a.g.w + e1) : 0u;
-          if ((m1 && a.op.visit(acc1, (int32_t)v1, u1, w)) || ++e1 >= h1) d1 = true;
+        acc[k] = a.op.init();
+        done[k] = e[k] >= h[k];
+      }
+      while (true) {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < kPullK; ++k) any |= !done[k];
+        if (!any) break;
+        int32_t u[kPullK];
+#pragma unroll
+        for (int k = 0; k < kPullK; ++k) u[k] = done[k] ? 0 : __ldg(a.g.nbr + e[k]);
+        bool m[kPullK];
+#pragma unroll
+        for (int k = 0; k < kPullK; ++k) m[k] = !done[k] && a.in.member(u[k]);
+#pragma unroll
+        for (int k = 0; k < kPullK; ++k) {
+          if (done[k]) continue;
+          const uint32_t w = a.g.w ? __ldg(a.g.w + e[k]) : 0u;
+          if ((m[k] && a.op.visit(acc[k], (int32_t)(v0 + k * nth), u[k], w)) || ++e[k] >= h[k]) done[k] = true;
         }
       }
-      if (a0) a.op.finish((int32_t)v0, acc0, a.out);
-      if (a1) a.op.finish((int32_t)v1, acc1, a.out);
+#pragma unroll
+      for (int k = 0; k < kPullK; ++k)
+        if (act[k]) a.op.finish((int32_t)(v0 + k * nth), acc[k], a.out);
     }
     add_scanned(a.scanned, sc);
     return;
