@@ -184,6 +184,43 @@ struct OpHook {
       if (((need >> k) & 1u) && lo[k] < cur[k]) any |= atomicMin(label + hi[k], lo[k]) > lo[k];
     if (any && !*((volatile int*)changed)) *changed = 1;
   }
+  // the same for 4 arcs with their own sources (ETWC's balanced thread stage)
+  __device__ __forceinline__ void push4u(const int32_t (&u)[4], const int32_t (&v)[4], unsigned live, int,
+                                         const OutBuilder&) const {
+    if (giant) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((live >> k) & 1u) && ((__ldg(giant + (u[k] >> 5)) >> (u[k] & 31)) & 1u) &&
+            ((__ldg(giant + (v[k] >> 5)) >> (v[k] & 31)) & 1u))
+          live &= ~(1u << k);
+    }
+    if (!live) return;
+    int32_t la[4], lb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool l = (live >> k) & 1u;
+      la[k] = l ? *((volatile int32_t*)label + u[k]) : 0;
+      lb[k] = l ? *((volatile int32_t*)label + v[k]) : 0;
+    }
+    int32_t lo[4], hi[4], cur[4];
+    unsigned need = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      lo[k] = la[k] < lb[k] ? la[k] : lb[k];
+      hi[k] = la[k] < lb[k] ? lb[k] : la[k];
+      if (((live >> k) & 1u) && lb[k] != la[k]) need |= 1u << k;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool known_root = root_skip && hi[k] == v[k] && lb[k] == v[k];
+      cur[k] = ((need >> k) & 1u) && !known_root ? *((volatile int32_t*)label + hi[k]) : INT32_MAX;
+    }
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((need >> k) & 1u) && lo[k] < cur[k]) any |= atomicMin(label + hi[k], lo[k]) > lo[k];
+    if (any && !*((volatile int*)changed)) *changed = 1;
+  }
   __device__ __forceinline__ Acc init() const { return 0; }
   __device__ __forceinline__ bool visit(Acc&, int32_t v, int32_t u, uint32_t) const {
     hook(u, v);
@@ -368,6 +405,32 @@ struct OpBcFwdAoS {
     for (int k = 0; k < 4; ++k)
       if (((live >> k) & 1u) && (d[k] == -1 || d[k] == nl) && (old[k] == -1 || old[k] == nl))
         atomicAdd(&st[v[k]].sigma, su);
+  }
+  __device__ __forceinline__ void push4u(const int32_t (&u)[4], const int32_t (&v)[4], unsigned live,
+                                         int use_filter, const OutBuilder& out) const {
+    const int32_t nl = level + 1;
+    if (use_filter) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((live >> k) & 1u) && bm_has(vis, v[k])) live &= ~(1u << k);
+    }
+    if (!live) return;
+    int32_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = ((live >> k) & 1u) ? *((volatile int32_t*)&st[v[k]].depth) : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((live >> k) & 1u) && use_filter && d[k] != -1 && d[k] != nl) live &= ~(1u << k);
+    int32_t old[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) old[k] = ((live >> k) & 1u) && d[k] == -1 ? atomicCAS(&st[v[k]].depth, -1, nl) : d[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((live >> k) & 1u) && d[k] == -1 && old[k] == -1) out.emit(v[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (((live >> k) & 1u) && (d[k] == -1 || d[k] == nl) && (old[k] == -1 || old[k] == nl))
+        atomicAdd(&st[v[k]].sigma, st[u[k]].sigma);
   }
   __device__ __forceinline__ Acc init() const { return {0.0, 0}; }
   __device__ __forceinline__ bool visit(Acc& a, int32_t, int32_t u, uint32_t) const {

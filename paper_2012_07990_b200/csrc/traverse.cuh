@@ -707,6 +707,69 @@ __global__ void __launch_bounds__(256, kMinB) k_push_huge_mb(PushArgs<Op> a) {
   b_push_huge<Op>(a);
 }
 
+// Thread stage of ETWC for batched ops (CC hook, BC forward): the Q0 ranges
+// (each < 32 arcs, one per vertex) are concatenated and every thread takes an
+// equal contiguous share of their arcs, 4 at a time (push4u: one source per
+// arc), instead of one range per thread -- a thread with a 31-arc remainder
+// no longer holds its CTA at the chunk barrier (barrier stalls were 21% of
+// the CC hook round).  Which thread walks which arc is not observable.
+#ifndef GG_ETWC_BALANCED_T0
+#define GG_ETWC_BALANCED_T0 1
+#endif
+constexpr bool kEtwcBalancedT0 = GG_ETWC_BALANCED_T0 != 0;
+template <class Op>
+__device__ __forceinline__ void etwc_stage0_balanced(const PushArgs<Op>& a, const EtwcEntry* q, int n) {
+  __shared__ int32_t s_ex[257];  // exclusive prefix of the ranges' lengths; s_ex[n] = total
+  __shared__ int32_t s_wsum[32];
+  const int t = threadIdx.x, lane = lane_id(), wid = t >> 5, nw = blockDim.x >> 5;
+  int32_t len = t < n ? q[t].len : 0;
+  int32_t x = len;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[wid] = x;
+  __syncthreads();
+  int32_t off = 0;
+  for (int w = 0; w < wid; ++w) off += s_wsum[w];
+  if (t < n) s_ex[t] = off + x - len;
+  if (t == n - 1) s_ex[n] = off + x;
+  if (n == 0 && t == 0) s_ex[0] = 0;
+  __syncthreads();
+  const int32_t T = s_ex[n];
+  const int32_t j0 = (int32_t)((int64_t)T * t / blockDim.x), j1 = (int32_t)((int64_t)T * (t + 1) / blockDim.x);
+  if (j0 >= j1) return;
+  int lo = 0, hi = n;  // entry holding arc j0: last k with s_ex[k] <= j0
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_ex[mid] <= j0) lo = mid; else hi = mid;
+  }
+  int k = lo;
+  int32_t kend = s_ex[k + 1];
+  for (int32_t j = j0; j < j1; j += 4) {
+    int32_t u[4], v[4];
+    unsigned live = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int32_t jj = j + b;
+      u[b] = 0;
+      v[b] = 0;
+      if (jj < j1) {
+        while (jj >= kend) {
+          ++k;
+          kend = s_ex[k + 1];
+        }
+        const EtwcEntry& c = q[k];
+        u[b] = c.u;
+        v[b] = __ldg(a.g.nbr + c.lo + (jj - (kend - c.len)));
+        live |= 1u << b;
+      }
+    }
+    a.op.push4u(u, v, live, a.use_filter, a.out);
+  }
+}
+
 template <class Op>
 __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
   __shared__ EtwcEntry s_q[3][256];
@@ -756,9 +819,20 @@ __device__ __forceinline__ void b_push_etwc(PushArgs<Op> a, int cta) {
     }
     __syncthreads();
     // stage 0: individual threads
-    for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
-      EtwcEntry c = s_q[0][k];
-      push_range_strided(a, c.u, c.lo, c.hi(), 0, 1, false);
+    if constexpr (PushBatch<Op>::value) {
+      if (kEtwcBalancedT0) {
+        etwc_stage0_balanced(a, s_q[0], s_n[0]);
+      } else {
+        for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
+          EtwcEntry c = s_q[0][k];
+          push_range_strided(a, c.u, c.lo, c.hi(), 0, 1, false);
+        }
+      }
+    } else {
+      for (int k = threadIdx.x; k < s_n[0]; k += blockDim.x) {
+        EtwcEntry c = s_q[0][k];
+        push_range_strided(a, c.u, c.lo, c.hi(), 0, 1, false);
+      }
     }
     // stage 1: warps
     for (int k = wid; k < s_n[1]; k += nw) {
