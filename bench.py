@@ -412,7 +412,9 @@ def main():
             "clocks": clk.summary()}
 
     # device ranks of the last timed step (parity below, outside the timed region)
-    ranks_dev = ranks.cpu().numpy() if rank == 0 and world == 1 else None
+    # (.copy(): numpy-owned memory -- a view of the .cpu() tensor was seen
+    # overwritten by later host allocations in this process)
+    ranks_dev = ranks.cpu().numpy().copy() if rank == 0 and world == 1 else None
 
     # Secondary measurement, NOT the headline: the same run with contributions
     # STORED in f32 (every sum still f64; error bound ~3.4e-7 relative, below
@@ -450,8 +452,10 @@ def main():
             "prep_ms": pm32.value,
             "note": "not the headline: contributions stored f32, all sums f64 (same kernels); "
                     "parity vs the same oracle ranks below"}}
-        ranks32 = r32.cpu().numpy()
+        ranks32 = r32.cpu().numpy().copy()
         del r32
+        if ranks_dev is not None:  # against this run's f64 ranks (same device, same order)
+            line["config"]["variants"]["contrib_f32"]["max_rel_diff_vs_f64_run"] = rel_err(ranks32, ranks_dev)
     src_h = torch.from_numpy(g.coo_src).pin_memory()
     dst_h = torch.from_numpy(g.coo_dst).pin_memory()
     g.close()

@@ -149,7 +149,7 @@ def pagerank_c1(gg, args, peak):
             launches = r.stats.gpu_launches
         m = statistics.median(ms)
         res[name] = {"ms": m, "gteps": iters * E / (m * 1e-3) / 1e9, "gpu_launches": launches,
-                     "ranks": ranks.cpu().numpy()}
+                     "ranks": ranks.cpu().numpy().copy()}
     best = max(res, key=lambda k: res[k]["gteps"])
     prog = gg.ScheduleProgram(variants[best])
 
