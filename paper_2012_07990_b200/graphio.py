@@ -67,7 +67,14 @@ class Graph:
                                       or dst.max() >= num_vertices):
             raise GraphLoadError("vertex id out of range [0, %d)" % num_vertices)
         w = None
-        if weights is not None:
+        if (isinstance(weights, np.ndarray) and weights.dtype == np.uint32
+                and weights.flags.c_contiguous):
+            # already the device's weight type: in range by construction,
+            # uploaded as-is (no host passes over the arcs)
+            if weights.shape != src.shape:
+                raise GraphLoadError("weights length mismatch")
+            w = weights
+        elif weights is not None:
             w64 = np.asarray(weights, dtype=np.int64)
             if w64.shape != src.shape:
                 raise GraphLoadError("weights length mismatch")

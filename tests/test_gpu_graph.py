@@ -144,3 +144,24 @@ def test_reference_written_sidecar_to_device():
                                                             blocking=True, blocking_size=n)})
             r = gg.pagerank(graph, prog, max_iters=15, tolerance=0.0).array
             assert np.max(np.abs(r - want_pr) / want_pr) < 1e-12
+
+
+def test_uint32_weights_uploaded_as_is(gg):
+    """uint32 weights skip the host range passes (graphio.from_coo fast path):
+    same device graph and SSSP distances as the checked int64 path; a length
+    mismatch is still rejected."""
+    import numpy as np
+    from paper_2012_07990_b200.graphio import GraphLoadError
+    rng = np.random.default_rng(3)
+    V = 500
+    s = rng.integers(0, V, 4000).astype(np.int32)
+    d = rng.integers(0, V, 4000).astype(np.int32)
+    w = rng.integers(0, 2**20, 4000).astype(np.uint32)
+    g1 = gg.Graph.from_coo(V, s, d, w)
+    g2 = gg.Graph.from_coo(V, s, d, w.astype(np.int64))
+    assert np.array_equal(np.asarray(g1.out_weights), np.asarray(g2.out_weights))
+    r1 = gg.sssp_delta(g1, 0)
+    r2 = gg.sssp_delta(g2, 0)
+    assert np.array_equal(r1.array, r2.array)
+    with pytest.raises(GraphLoadError):
+        gg.Graph.from_coo(V, s, d, w[:-1])
