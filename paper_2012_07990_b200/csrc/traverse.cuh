@@ -582,20 +582,20 @@ __device__ __forceinline__ void push_range_strided(const PushArgs<Op>& a, int32_
       }
       a.op.push4(u, v, live, a.use_filter, a.out);  // applies the filter itself, batched
     }
-    return;
-  }
-  for (; e + 3 * stride < hi; e += 4 * stride) {
-    int32_t v[4];
+  } else {
+    for (; e + 3 * stride < hi; e += 4 * stride) {
+      int32_t v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = __ldg(a.g.nbr + e + k * stride);
+      for (int k = 0; k < 4; ++k) v[k] = __ldg(a.g.nbr + e + k * stride);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (a.use_filter && !a.op.filter(v[k])) continue;
-      uint32_t w = a.g.w ? __ldg(a.g.w + e + k * stride) : 0u;
-      a.op.push(u, v[k], w, a.out);
+      for (int k = 0; k < 4; ++k) {
+        if (a.use_filter && !a.op.filter(v[k])) continue;
+        uint32_t w = a.g.w ? __ldg(a.g.w + e + k * stride) : 0u;
+        a.op.push(u, v[k], w, a.out);
+      }
     }
+    for (; e < hi; e += stride) push_edge(a, u, e);
   }
-  for (; e < hi; e += stride) push_edge(a, u, e);
 }
 
 // Grid-wide pass over the CTA-stage ranges queued by b_push_etwc.  The
@@ -721,7 +721,7 @@ template <class Op>
 __device__ __forceinline__ void etwc_stage0_balanced(const PushArgs<Op>& a, const EtwcEntry* q, int n) {
   __shared__ int32_t s_ex[257];  // exclusive prefix of the ranges' lengths; s_ex[n] = total
   __shared__ int32_t s_wsum[32];
-  const int t = threadIdx.x, lane = lane_id(), wid = t >> 5, nw = blockDim.x >> 5;
+  const int t = threadIdx.x, lane = lane_id(), wid = t >> 5;
   int32_t len = t < n ? q[t].len : 0;
   int32_t x = len;  // inclusive warp scan
 #pragma unroll
