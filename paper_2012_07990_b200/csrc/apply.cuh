@@ -178,10 +178,15 @@ void run_edge_only(Runtime* rt, const gg_schedule& s, const Op& op, bool use_fil
     const int64_t* seg = b->seg_end.p;
     int64_t nseg = b->nseg;
     void* args[] = {&a, &seg, &nseg};
-    int blocks = max_coop_blocks((const void*)k_edge_blocked<Op>, 256, dev);
-    GG_CUDA(cudaLaunchCooperativeKernel((const void*)k_edge_blocked<Op>, blocks, 256, args, 0, st));
+    const void* fn = (const void*)k_edge_blocked<Op>;
+    if constexpr (MinBlocks<Op>::value > 1) fn = (const void*)k_edge_blocked_mb<Op, MinBlocks<Op>::value>;
+    int blocks = max_coop_blocks(fn, 256, dev);
+    GG_CUDA(cudaLaunchCooperativeKernel(fn, blocks, 256, args, 0, st));
   } else {
-    k_edge_only<Op><<<grid_for(g->E / 4 + 1, 256, dev, 16), 256, 0, st>>>(a);
+    if constexpr (MinBlocks<Op>::value > 1)
+      k_edge_only_mb<Op, MinBlocks<Op>::value><<<grid_for(g->E / 4 + 1, 256, dev, 16), 256, 0, st>>>(a);
+    else
+      k_edge_only<Op><<<grid_for(g->E / 4 + 1, 256, dev, 16), 256, 0, st>>>(a);
     GG_LAUNCH_CHECK();
   }
   count_launch();

@@ -1260,10 +1260,19 @@ __device__ __forceinline__ void edge_range(const EdgeArgs<Op>& a, int64_t lo, in
   for (int64_t k = tid; k < nvec; k += nthreads) {
     int4 s = ld_stream4(s4 + k), d = ld_stream4(d4 + k);
     int64_t e = head + 4 * k;
-    edge_one(a, s.x, d.x, e);
-    edge_one(a, s.y, d.y, e + 1);
-    edge_one(a, s.z, d.z, e + 2);
-    edge_one(a, s.w, d.w, e + 3);
+    if constexpr (PushBatch<Op>::value) {  // the 4 arcs' chains in flight together
+      const int32_t uu[4] = {s.x, s.y, s.z, s.w}, vv[4] = {d.x, d.y, d.z, d.w};
+      unsigned live = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (a.in.member(uu[q])) live |= 1u << q;
+      a.op.push4u(uu, vv, live, a.use_filter, a.out);
+    } else {
+      edge_one(a, s.x, d.x, e);
+      edge_one(a, s.y, d.y, e + 1);
+      edge_one(a, s.z, d.z, e + 2);
+      edge_one(a, s.w, d.w, e + 3);
+    }
   }
   for (int64_t e = head + 4 * nvec + tid; e < hi; e += nthreads)
     edge_one(a, __ldg(a.coo.src + e), __ldg(a.coo.dst + e), e);
@@ -1276,6 +1285,10 @@ __device__ __forceinline__ void b_edge_only(EdgeArgs<Op> a) {
 }
 template <class Op>
 __global__ void __launch_bounds__(256) k_edge_only(EdgeArgs<Op> a) {
+  b_edge_only<Op>(a);
+}
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_edge_only_mb(EdgeArgs<Op> a) {
   b_edge_only<Op>(a);
 }
 
@@ -1299,6 +1312,11 @@ __device__ __forceinline__ void b_edge_blocked(EdgeArgs<Op> a, const int64_t* se
 template <class Op>
 __global__ void __launch_bounds__(256) k_edge_blocked(EdgeArgs<Op> a, const int64_t* seg_end,
                                                       int64_t nseg) {
+  b_edge_blocked<Op>(a, seg_end, nseg);
+}
+template <class Op, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) k_edge_blocked_mb(EdgeArgs<Op> a, const int64_t* seg_end,
+                                                                int64_t nseg) {
   b_edge_blocked<Op>(a, seg_end, nseg);
 }
 
